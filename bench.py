@@ -1,0 +1,381 @@
+"""Benchmark of the k-clique counting hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload rmat18] [--k 7] [--algo orient] [--scheme vertex]
+                    [--criterion degeneracy]
+
+A *step* is one pass of the reference's counting path over one synthetic
+graph: ``run_count(g, cfg)`` = device degree/k-core ranking + orientation +
+induced-bitmap extraction + traversal + exact reduction (the reference's
+``orient_ms + count_ms``, PAPER.md:568 -- graph load excluded).  ``value`` is
+k-cliques/s with the undirected CSR already resident in HBM; ``e2e`` is the
+same metric through the public API from pinned host edge pairs
+(``from_edges`` + ``run_count``, H2D of the pairs and D2H of the result inside
+the timed region).  N>1: one process per GPU (torchrun), root-range shards,
+one NCCL u64 all-reduce of the raw partials (shard.py), max-over-ranks time.
+
+``--impl reference`` times the CPU restatement of the reference (oracle/,
+C + pthreads, every host core) on a bounded task sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+
+# BASELINE.json configs[1]: RMAT scale-18 ef16, degeneracy orientation, 1 GPU
+DEFAULTS = dict(workload="rmat18", k=7, algo="orient", scheme="vertex", criterion="degeneracy")
+METRIC = "k-cliques/sec"
+FLUSH_BYTES = 512 << 20  # > 126 MB L2
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--workload", default=DEFAULTS["workload"])
+    ap.add_argument("--k", type=int, default=DEFAULTS["k"])
+    ap.add_argument("--algo", default=DEFAULTS["algo"])
+    ap.add_argument("--scheme", default=DEFAULTS["scheme"])
+    ap.add_argument("--criterion", default=DEFAULTS["criterion"])
+    ap.add_argument("--group", type=int, default=0)
+    ap.add_argument("--cpu-sample-s", type=float, default=12.0,
+                    help="target CPU seconds of the oracle baseline sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def workload_edges(name):
+    from paper_2104_13209_b200 import synth
+
+    cache = os.environ.get("KC_GRAPH_CACHE")
+    if cache:
+        p = os.path.join(cache, f"{name}.npy")
+        if os.path.exists(p):
+            return np.load(p)
+    e = synth.workload(name)
+    if cache:
+        os.makedirs(cache, exist_ok=True)
+        np.save(os.path.join(cache, f"{name}.npy"), e)
+    return e
+
+
+def config_dict(a, world):
+    return {"workload": a.workload, "k": a.k, "algorithm": a.algo, "scheme": a.scheme,
+            "criterion": a.criterion, "group_size": a.group,
+            "parallelism": f"root-range shards x{world}" if world > 1 else "1 GPU",
+            "l2": "flushed between timed steps (512 MiB write)",
+            "step": "run_count: rank + orient + extract + traverse + exact reduce"}
+
+
+# ----------------------------------------------------------------------------
+# dist helpers
+# ----------------------------------------------------------------------------
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, val in zip(names, f[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------
+# our arm
+# ----------------------------------------------------------------------------
+def count_kernel_launches(step):
+    """Kernels launched by one step, counted by CUPTI through torch.profiler."""
+    try:
+        import torch
+        from torch.profiler import ProfilerActivity, profile
+
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            step()
+            torch.cuda.synchronize()
+        names = {}
+        for ev in prof.events():
+            if ev.device_type.name == "CUDA" and not ev.name.startswith("Memcpy") \
+                    and not ev.name.startswith("Memset"):
+                names[ev.name] = names.get(ev.name, 0) + 1
+        return sum(names.values()), names
+    except Exception as exc:  # profiler unavailable: report unknown
+        return None, {"error": str(exc)[:200]}
+
+
+def run_ours(a):
+    import torch
+    import torch.distributed as dist
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    os.environ["KC_DEVICE"] = str(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import paper_2104_13209_b200 as kc
+    from paper_2104_13209_b200 import _lib
+    from paper_2104_13209_b200.orientation import rank_and_orient
+    from paper_2104_13209_b200.shard import balanced_ranges, run_count_sharded, task_costs
+
+    _lib.load()
+    edges = workload_edges(a.workload)
+    g = kc.from_edges(edges, device=local)
+    cfg = kc.RunConfig(k=a.k, algorithm=a.algo, scheme=a.scheme, criterion=a.criterion,
+                       group_size=a.group)
+
+    def step(graph=g):
+        if world > 1:
+            return run_count_sharded(graph, cfg, rank, world)
+        return kc.run_count(graph, cfg)
+
+    stream = torch.cuda.ExternalStream(_lib.graph_stream(g.handle), device=local)
+    flush = torch.empty(FLUSH_BYTES // 4, dtype=torch.int32, device=f"cuda:{local}")
+    rep = None
+    for _ in range(max(a.warmup, 0)):
+        rep = step()
+    n_launch, launch_names = count_kernel_launches(step) if rank == 0 else (None, {})
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
+    phase = {"orient_ms": [], "count_ms": [], "device_count_ms": []}
+    with Clocks(local) as clk:
+        barrier()
+        for i in range(a.steps):
+            flush.fill_(i)                       # L2 flush (outside the timed events)
+            torch.cuda.synchronize()
+            starts[i].record(stream)
+            rep = step()
+            ends[i].record(stream)
+            torch.cuda.synchronize()
+            phase["orient_ms"].append(rep.orient_ms)
+            phase["count_ms"].append(rep.count_ms)
+            phase["device_count_ms"].append((rep.device_ms or {}).get("count", 0.0))
+        barrier()
+    ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    total_ms = float(sum(ms))
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    count = rep.count
+    value = count * a.steps / (total_ms / 1e3)
+
+    # e2e: public API from pinned host pairs (H2D in the timed region)
+    e2e = None
+    if not a.no_e2e:
+        pinned = torch.from_numpy(np.ascontiguousarray(edges)).pin_memory()
+        host_edges = pinned.numpy()
+        d2h = 8 * 8 + 8 * 1024 + (8 * (rep.d_max + 2) ** 2 if a.algo == "pivot" else 0)
+
+        def e2e_step():
+            gg = kc.from_edges(host_edges, device=local)
+            r = step(gg)
+            gg.free()
+            return r
+
+        e2e_step()
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(a.steps):
+            r = e2e_step()
+            assert r.count == count
+        torch.cuda.synchronize()
+        e_ms = (time.perf_counter() - t0) * 1e3
+        if world > 1:
+            t = torch.tensor([e_ms], dtype=torch.float64, device=f"cuda:{local}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t.item())
+        e2e = {"value": count * a.steps / (e_ms / 1e3), "unit": "k-cliques/s",
+               "ms_per_step": e_ms / a.steps, "h2d_bytes_per_step": int(edges.nbytes),
+               "d2h_bytes_per_step": int(d2h), "timer": "host wall clock, synced"}
+
+    roof = roofline(kc, g, cfg, rep, a, local) if rank == 0 else None
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        cpu = cpu_baseline(edges, a, count, target_s=a.cpu_sample_s)
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "k-cliques/s", "n_gpus": world,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": total_ms / a.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "u32 bitmaps / u64 counts (integer)", "data": "synthetic (seeded generator)",
+            "config": config_dict(a, world), "count": str(count),
+            "phases_ms": {k: float(np.median(v)) for k, v in phase.items()},
+            "d_max": rep.d_max, "degeneracy": rep.degeneracy, "visits": rep.load.total,
+            "normalized_max": rep.load.normalized_max, "step_ms": ms,
+            "clocks": clk.summary(), "e2e": e2e, "gpu_launches": (n_launch * a.steps
+                                                                  if n_launch else None),
+            "gpu_launches_per_step": n_launch, "kernels": launch_names,
+            "roofline": roof, "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def roofline(kc, g, cfg, rep, a, local):
+    """Roofline of the dominant kernel (k_count) from an instrumented re-run.
+
+    ALU bound: algorithmic word-ops = sum over expanded tree nodes of the
+    u32 words of the row AND+POPC'd; the peak is the
+    measured sustained AND+POPC word rate of this GPU (kc_microbench).
+    """
+    try:
+        from paper_2104_13209_b200 import profile as kprof
+    except ImportError:
+        return None
+    try:
+        return kprof.roofline(g, cfg, rep)
+    except Exception as exc:
+        return {"error": str(exc)[:300]}
+
+
+# ----------------------------------------------------------------------------
+# CPU baseline / reference arm: the C restatement of the reference
+# ----------------------------------------------------------------------------
+def cpu_baseline(edges, a, full_count=None, target_s=12.0, workers=None):
+    """Oracle (C + pthreads) on a contiguous task range sized to ~target_s.
+
+    Throughput = cliques counted in the sample / (sample count time +
+    sample-fraction of the full CPU ranking+orientation time)."""
+    import oracle
+
+    workers = workers or os.cpu_count() or 1
+    g = oracle.from_edges(edges)
+    t0 = time.perf_counter()
+    rank, degen = oracle.compute_rank(g, a.criterion)
+    og = oracle.orient(g, rank, degen)
+    orient_s = time.perf_counter() - t0
+    n_tasks = oracle.num_tasks(og, a.scheme)
+    span = max(1, n_tasks // 4096)
+    lo = 0
+    done_tasks, cnt, spent = 0, 0, 0.0
+    while spent < target_s and lo < n_tasks:
+        hi = min(n_tasks, lo + span)
+        t1 = time.perf_counter()
+        c, _, _ = oracle.run_tasks(og, a.k, a.algo, a.scheme, False, workers, lo, hi)
+        dt = time.perf_counter() - t1
+        cnt += c
+        spent += dt
+        done_tasks += hi - lo
+        lo = hi
+        if dt < target_s / 8:
+            span *= 2
+    frac = done_tasks / max(n_tasks, 1)
+    t_eff = spent + orient_s * frac
+    full = frac >= 1.0
+    return {"value": cnt / t_eff if t_eff > 0 else None, "unit": "k-cliques/s",
+            "cores": workers, "kind": "port",
+            "sample": (f"oracle/kc_oracle.c run_tasks on tasks [0,{done_tasks}) of {n_tasks} "
+                       f"({100 * frac:.3f}%), {spent:.1f}s count + {orient_s:.2f}s orient x frac"
+                       + ("; full graph" if full else "")),
+            "sample_count": str(cnt), "full_count_matches": (cnt == full_count) if full else None,
+            "orient_s_full": orient_s}
+
+
+def run_reference(a):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    edges = workload_edges(a.workload)
+    per = max(2.0, min(a.cpu_sample_s, 120.0 / max(a.steps + a.warmup, 1)))
+    for _ in range(a.warmup):
+        cpu_baseline(edges, a, target_s=per / 4)
+    vals, ms = [], []
+    last = None
+    for _ in range(a.steps):
+        t0 = time.perf_counter()
+        last = cpu_baseline(edges, a, target_s=per)
+        ms.append((time.perf_counter() - t0) * 1e3)
+        vals.append(last["value"])
+    value = float(np.median(vals))
+    cpu = dict(last)
+    cpu["value"] = value
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "k-cliques/s",
+        "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": float(np.mean(ms)), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "u64 bitmaps / u128 counts (integer)",
+        "data": "synthetic (seeded generator)", "config": config_dict(a, world),
+        "cpu_baseline": cpu,
+        "e2e": {"value": value, "unit": "k-cliques/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0}}), flush=True)
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)
+
+
+if __name__ == "__main__":
+    main()

@@ -79,6 +79,9 @@ int kc_graph_info(const kc_graph *g, int64_t *n, int64_t *m, int64_t *d_max_undi
 int kc_graph_download(const kc_graph *g, int64_t *row_ptr, int32_t *col, int32_t *coo_src,
                       int64_t *orig_ids);
 void kc_graph_free(kc_graph *g);
+/* the CUDA stream (cudaStream_t) every device call on this graph is issued
+ * on, so a caller can record its own events around the library's work */
+int kc_graph_stream(const kc_graph *g, void **stream);
 
 /* ---- orientation (orientation.py:116-153) ------------------------- */
 typedef struct {
@@ -124,6 +127,8 @@ typedef struct {
     int64_t hist_dim;       /* L: hist is L x L u64 (pivot), 0 for orient */
     double count_ms;        /* device time of the counting kernels */
     double extract_frac;    /* reserved */
+    uint64_t word_ops;      /* roofline: u32 row words ANDed (+POPC) by the traversals */
+    uint64_t extract_bytes; /* roofline: global bytes read by the sub-graph builder */
 } kc_count_raw;
 
 /* hist: caller buffer of hist_cap u64 (L*L, L = d_max + 2) or NULL for orient;
@@ -148,6 +153,11 @@ int kc_count_bitgraph(int device, const uint64_t *rows, int64_t d, int32_t t, in
 /* engine_pivot.py:82-114: argmax |cand & row(v)|, lowest id on ties */
 int kc_find_pivot(int device, const uint64_t *rows, int64_t d, const uint64_t *cand,
                   int64_t *pivot, uint64_t *pruned);
+
+/* ---- roofline probe ------------------------------ */
+/* measured full-chip AND+POPC word rate with register operands (reg_wps) and
+ * with one operand streamed from shared memory (smem_wps), words/s */
+int kc_probe(int device, double *reg_wps, double *smem_wps, double *sm_mhz);
 
 #ifdef __cplusplus
 }

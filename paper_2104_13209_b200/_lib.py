@@ -24,8 +24,8 @@ SCHEME = {"vertex": 0, "edge": 1}
 EXPORTS = (
     "kc_abi_version", "kc_last_error", "kc_device_count", "kc_num_sms",
     "kc_graph_from_edges", "kc_graph_from_csr", "kc_graph_info", "kc_graph_download",
-    "kc_graph_free", "kc_orient", "kc_dag_download", "kc_count", "kc_num_tasks",
-    "kc_task_costs", "kc_extract", "kc_count_bitgraph", "kc_find_pivot",
+    "kc_graph_free", "kc_graph_stream", "kc_orient", "kc_dag_download", "kc_count", "kc_num_tasks",
+    "kc_task_costs", "kc_extract", "kc_count_bitgraph", "kc_find_pivot", "kc_probe",
 )
 
 
@@ -45,7 +45,8 @@ class KcCountArgs(ctypes.Structure):
 class KcCountRaw(ctypes.Structure):
     _fields_ = [("limbs", ctypes.c_uint64 * 4), ("visits", ctypes.c_uint64),
                 ("tasks_run", ctypes.c_uint64), ("hist_dim", ctypes.c_int64),
-                ("count_ms", ctypes.c_double), ("extract_frac", ctypes.c_double)]
+                ("count_ms", ctypes.c_double), ("extract_frac", ctypes.c_double),
+                ("word_ops", ctypes.c_uint64), ("extract_bytes", ctypes.c_uint64)]
 
 
 class KcError(RuntimeError):
@@ -85,6 +86,7 @@ def load(path: str = LIB_PATH):
                                          ctypes.POINTER(_i64), ctypes.POINTER(ctypes.c_double)]),
         "kc_graph_download": (ctypes.c_int, [_P, _P, _P, _P, _P]),
         "kc_graph_free": (None, [_P]),
+        "kc_graph_stream": (ctypes.c_int, [_P, ctypes.POINTER(_P)]),
         "kc_orient": (ctypes.c_int, [_P, ctypes.c_int, _P, ctypes.POINTER(KcDagInfo)]),
         "kc_dag_download": (ctypes.c_int, [_P, _P, _P, _P, _P]),
         "kc_count": (ctypes.c_int, [_P, ctypes.POINTER(KcCountArgs), ctypes.POINTER(KcCountRaw),
@@ -95,6 +97,9 @@ def load(path: str = LIB_PATH):
                                       ctypes.POINTER(_i64)]),
         "kc_count_bitgraph": (ctypes.c_int, [ctypes.c_int, _P, _i64, _i32, _i32, _i32, _P, _P,
                                              _P]),
+        "kc_probe": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_double),
+                                    ctypes.POINTER(ctypes.c_double),
+                                    ctypes.POINTER(ctypes.c_double)]),
         "kc_find_pivot": (ctypes.c_int, [ctypes.c_int, _P, _i64, _P, ctypes.POINTER(_i64), _P]),
     }
     for name, (res, args) in sig.items():
@@ -126,6 +131,13 @@ def device_count() -> int:
 
 def num_sms(device: int = 0) -> int:
     return int(load().kc_num_sms(device))
+
+
+def graph_stream(handle) -> int:
+    """cudaStream_t (as an int) the library issues this graph's work on."""
+    s = ctypes.c_void_p()
+    check(load().kc_graph_stream(handle, ctypes.byref(s)))
+    return int(s.value or 0)
 
 
 def current_device() -> int:

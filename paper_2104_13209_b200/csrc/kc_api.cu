@@ -157,6 +157,21 @@ int kc_graph_download(const kc_graph *g, int64_t *row_ptr, int32_t *col, int32_t
 
 void kc_graph_free(kc_graph *g) { destroy(g); }
 
+int kc_probe(int device, double *reg_wps, double *smem_wps, double *sm_mhz) {
+    return guarded([&] {
+        KC_REQUIRE(reg_wps && smem_wps && sm_mhz, KC_EINVAL, "NULL output");
+        require_device(device);
+        kc_do_probe(device, reg_wps, smem_wps, sm_mhz);
+    });
+}
+
+int kc_graph_stream(const kc_graph *g, void **stream) {
+    return guarded([&] {
+        KC_REQUIRE(g && stream, KC_EINVAL, "graph or stream is NULL");
+        *stream = reinterpret_cast<void *>(g->stream);
+    });
+}
+
 int kc_orient(kc_graph *g, int criterion, const int32_t *rank_in, kc_dag_info *info) {
     return guarded([&] {
         KC_REQUIRE(g, KC_EINVAL, "graph is NULL");

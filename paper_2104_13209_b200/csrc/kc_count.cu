@@ -64,6 +64,8 @@ struct CountParams {
     ull *task_counter;
     ull *limbs;          // [4]
     ull *visits_total;
+    ull *word_ops;       // roofline counters (kc_count_raw.word_ops / extract_bytes)
+    ull *ext_bytes;
     ull *visits_per_sm;
     ull *tasks_run;
 };
@@ -111,7 +113,7 @@ __device__ __forceinline__ int smem_find(const int32_t *a, int n, int32_t x) {
 template <int BLOCK>
 __device__ int build_task(const CountParams &p, int32_t task, int32_t *l2g, uint32_t *rows,
                           int32_t *scratch, bool need_rows, bool directed, int *s_cnt,
-                          int *s_warp) {
+                          int *s_warp, ull &bytes) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     constexpr int NW = BLOCK / 32;
     int d;
@@ -120,6 +122,7 @@ __device__ int build_task(const CountParams &p, int32_t task, int32_t *l2g, uint
         const int64_t beg = p.orow[task];
         d = int(p.orow[task + 1] - beg);
         for (int i = tid; i < d; i += BLOCK) l2g[i] = p.ocol[beg + i];
+        if (tid == 0) bytes += 4 /*task id*/ + 16 + 4ull * d;
     } else {
         // bitgraph.py:67-86 locals = common out-neighbours of (src, dst);
         // the longer list is staged in smem, the shorter one is probed
@@ -130,6 +133,7 @@ __device__ int build_task(const CountParams &p, int32_t task, int32_t *l2g, uint
             ab = bb; ae = be; bb = t0; be = t1;
         }
         const int la = int(ae - ab), lb = int(be - bb);
+        if (tid == 0) bytes += 4 + 8 + 32 + 4ull * (la + lb);
         for (int i = tid; i < lb; i += BLOCK) scratch[i] = p.ocol[bb + i];
         if (tid == 0) *s_cnt = 0;
         __syncthreads();
@@ -152,6 +156,7 @@ __device__ int build_task(const CountParams &p, int32_t task, int32_t *l2g, uint
     for (int i = warp; i < d; i += NW) {
         const int32_t gi = l2g[i];
         const int64_t beg = p.orow[gi], end = p.orow[gi + 1];
+        if (lane == 0) bytes += 16 + 4ull * (end - beg);
         for (int64_t e = beg + lane; e < end; e += 32) {
             const int32_t x = p.ocol[e];
             if (x < lo_id || x > hi_id) continue;
@@ -183,7 +188,8 @@ __device__ int load_given(const CountParams &p, uint32_t *rows) {
 // block reductions for the K8 epilogue
 // ---------------------------------------------------------------------------
 template <int BLOCK>
-__device__ void flush_block(const CountParams &p, ull acc, ull visits, ull tasks, ull *s_red) {
+__device__ void flush_block(const CountParams &p, ull acc, ull visits, ull tasks, ull work,
+                            ull bytes, ull *s_red) {
     constexpr int NW = BLOCK / 32;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     ull lo = acc & 0xffffffffull, hi = acc >> 32;
@@ -192,9 +198,13 @@ __device__ void flush_block(const CountParams &p, ull acc, ull visits, ull tasks
         hi += __shfl_xor_sync(0xffffffffu, hi, o);
         visits += __shfl_xor_sync(0xffffffffu, visits, o);
         tasks += __shfl_xor_sync(0xffffffffu, tasks, o);
+        work += __shfl_xor_sync(0xffffffffu, work, o);
+        bytes += __shfl_xor_sync(0xffffffffu, bytes, o);
     }
     __syncthreads();
     if (lane == 0) {
+        if (work && p.word_ops) atomicAdd(p.word_ops, work);
+        if (bytes && p.ext_bytes) atomicAdd(p.ext_bytes, bytes);
         s_red[4 * warp + 0] = lo;
         s_red[4 * warp + 1] = hi;
         s_red[4 * warp + 2] = visits;
@@ -238,7 +248,7 @@ __host__ __device__ __forceinline__ int group_stride(int frames, int W, int G) {
 
 template <int BLOCK>
 __device__ void orient_task(const CountParams &p, const uint32_t *rows, int d, uint32_t *stack,
-                            int *s_next, ull &acc, ull &visits) {
+                            int *s_next, ull &acc, ull &visits, ull &work) {
     const int t = p.t;
     const int tid = threadIdx.x, lane = tid & 31;
     const int W = (d + 31) >> 5, RS = row_stride(W);
@@ -265,7 +275,10 @@ __device__ void orient_task(const CountParams &p, const uint32_t *rows, int d, u
         u = __shfl_sync(gmask, u, 0, G);
         if (u >= d) break;
         // frame 0 expands u (engine_orient.py:58-62); S0 = all locals
-        if (gl == 0) ++visits;
+        if (gl == 0) {
+            ++visits;
+            work += W;
+        }
         const uint32_t *ru = rows + u * RS;
         if (last == 0) {
             for (int w = gl; w < W; w += G) acc += __popc(ru[w]);
@@ -304,7 +317,10 @@ __device__ void orient_task(const CountParams &p, const uint32_t *rows, int d, u
                 --s;
                 continue;
             }
-            if (gl == 0) ++visits;
+            if (gl == 0) {
+                ++visits;
+                work += W;
+            }
             const uint32_t *rv = rows + v * RS;
             const uint32_t *cs = cand(s);
             if (s == last) {
@@ -347,7 +363,7 @@ struct PivotFrames {
 // argmax_{c in cand} |cand & row(c)|, lowest c on ties (engine_pivot.py:82-101).
 // Whole warp; candidates compacted into `list`, scored lane-parallel.
 __device__ int warp_select_pivot(const uint32_t *rows, int RS, int W, const uint32_t *cand,
-                                 int *list) {
+                                 int *list, ull &work) {
     const int lane = threadIdx.x & 31;
     int n_c = 0;
     for (int c0 = 0; c0 < W; c0 += 32) {
@@ -366,6 +382,7 @@ __device__ int warp_select_pivot(const uint32_t *rows, int RS, int W, const uint
         n_c += __shfl_sync(0xffffffffu, incl, 31);
     }
     __syncwarp();
+    if (lane == 0) work += ull(n_c) * W;
     ull best = 0;
     for (int i = lane; i < n_c; i += 32) {
         const int c = list[i];
@@ -390,7 +407,8 @@ __device__ __forceinline__ void hist_add(const CountParams &p, ull *s_hist, int 
 
 // DFS of one root branch v0 (already expanded at frame 0 into frame 1 = child)
 __device__ void pivot_dfs(const CountParams &p, const uint32_t *rows, int RS, int W,
-                          const PivotFrames &F, int *list, ull *s_hist, ull &visits) {
+                          const PivotFrames &F, int *list, ull *s_hist, ull &visits,
+                          ull &work) {
     const int lane = threadIdx.x & 31;
     const int t = p.t;
     const bool allk = p.all_k != 0;
@@ -423,7 +441,10 @@ __device__ void pivot_dfs(const CountParams &p, const uint32_t *rows, int RS, in
         }
         const int np2 = npv + (v == piv ? 1 : 0);
         if (!allk && s + 1 - t > np2) continue;  // engine_pivot.py:152-153
-        if (lane == 0) ++visits;
+        if (lane == 0) {
+            ++visits;
+            work += W;
+        }
         const uint32_t *rv = rows + v * RS;
         uint32_t *fn = F.f(s + 1);
         uint32_t *Cn = fn;
@@ -441,7 +462,7 @@ __device__ void pivot_dfs(const CountParams &p, const uint32_t *rows, int RS, in
         const bool any = __ballot_sync(0xffffffffu, nz != 0) != 0;
         __syncwarp();
         if (any) {
-            const int pv = warp_select_pivot(rows, RS, W, Cn, list);
+            const int pv = warp_select_pivot(rows, RS, W, Cn, list, work);
             const uint32_t *rp = rows + pv * RS;
             for (int w = lane; w < W; w += 32) {
                 uint32_t y = Cn[w] & ~rp[w];
@@ -464,7 +485,7 @@ __device__ void pivot_dfs(const CountParams &p, const uint32_t *rows, int RS, in
 template <int BLOCK>
 __device__ void pivot_task(const CountParams &p, const uint32_t *rows, int d, uint32_t *pv_area,
                            int *lists, ull *s_hist, int *s_next, int *s_piv0, ull *s_key,
-                           ull &visits) {
+                           ull &visits, ull &work) {
     constexpr int NW = BLOCK / 32;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int W = (d + 31) >> 5, RS = row_stride(W);
@@ -519,7 +540,10 @@ __device__ void pivot_task(const CountParams &p, const uint32_t *rows, int d, ui
         if (!((P0[v >> 5] >> (v & 31)) & 1u)) continue;
         const int np2 = v == piv0 ? 1 : 0;
         if (!allk && 1 - t > np2) continue;
-        if (lane == 0) ++visits;
+        if (lane == 0) {
+            ++visits;
+            work += W;
+        }
         const uint32_t *rv = rows + v * RS;
         uint32_t *f1 = F.f(1);
         const int vq = v >> 5;
@@ -538,7 +562,7 @@ __device__ void pivot_task(const CountParams &p, const uint32_t *rows, int d, ui
             if ((allk || 1 >= t) && lane == 0) hist_add(p, s_hist, 1, np2);
             continue;
         }
-        const int pv = warp_select_pivot(rows, RS, W, f1, list);
+        const int pv = warp_select_pivot(rows, RS, W, f1, list, work);
         const uint32_t *rp = rows + pv * RS;
         for (int w = lane; w < W; w += 32) {
             uint32_t y = f1[w] & ~rp[w];
@@ -551,7 +575,7 @@ __device__ void pivot_task(const CountParams &p, const uint32_t *rows, int d, ui
             f1[3 * W + 2] = 0u;
         }
         __syncwarp();
-        pivot_dfs(p, rows, RS, W, F, list, s_hist, visits);
+        pivot_dfs(p, rows, RS, W, F, list, s_hist, visits, work);
     }
 }
 
@@ -581,7 +605,7 @@ __global__ void __launch_bounds__(BLOCK) k_count(CountParams p) {
         rows = p.rows_global + int64_t(blockIdx.x) * p.rows_slot;
     }
     for (int i = tid; i < hist_cells; i += BLOCK) s_hist[i] = 0;
-    ull acc = 0, visits = 0, tasks = 0;
+    ull acc = 0, visits = 0, tasks = 0, work = 0, bytes = 0;
     const bool directed = MODE == MODE_ORIENT || (MODE == MODE_EXTRACT && p.directed_out);
     const int t = p.t;
     for (;;) {
@@ -602,7 +626,7 @@ __global__ void __launch_bounds__(BLOCK) k_count(CountParams p) {
             // int32 scratch for the edge scheme lives in the work area
             const bool need_rows = MODE == MODE_EXTRACT || MODE == MODE_PIVOT || t >= 2;
             d = build_task<BLOCK>(p, task, l2g, rows, reinterpret_cast<int32_t *>(area), need_rows,
-                                  directed, &s_cnt, s_warp);
+                                  directed, &s_cnt, s_warp, bytes);
         }
         if (MODE == MODE_EXTRACT) {
             const int W = (d + 31) >> 5, RS = row_stride(W);
@@ -626,12 +650,12 @@ __global__ void __launch_bounds__(BLOCK) k_count(CountParams p) {
             continue;
         }
         if (MODE == MODE_ORIENT) {
-            orient_task<BLOCK>(p, rows, d, area, &s_next, acc, visits);
+            orient_task<BLOCK>(p, rows, d, area, &s_next, acc, visits, work);
         } else {
             pivot_task<BLOCK>(p, rows, d, area, reinterpret_cast<int *>(
                                   area + 2 * ((d + 31) >> 5) +
                                   (BLOCK / 32) * p.pv_smem_frames * pv_frame_words((d + 31) >> 5)),
-                              s_hist, &s_next, &s_piv0, s_key, visits);
+                              s_hist, &s_next, &s_piv0, s_key, visits, work);
         }
     }
     __syncthreads();
@@ -648,7 +672,7 @@ __global__ void __launch_bounds__(BLOCK) k_count(CountParams p) {
             }
         }
     }
-    if (MODE != MODE_EXTRACT) flush_block<BLOCK>(p, acc, visits, tasks, s_red);
+    if (MODE != MODE_EXTRACT) flush_block<BLOCK>(p, acc, visits, tasks, work, bytes, s_red);
 }
 
 // ---------------------------------------------------------------------------
@@ -872,8 +896,8 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
     DevBuf tasks;
     const int64_t n_tasks = build_tasks(g, a->scheme, lo, hi, min_d, tasks);
 
-    DevBuf outs(8 * (8 + size_t(kSmidSlots)));
-    KC_CUDA(cudaMemsetAsync(outs.p, 0, 8 * (8 + size_t(kSmidSlots)), g->stream));
+    DevBuf outs(8 * (10 + size_t(kSmidSlots)));
+    KC_CUDA(cudaMemsetAsync(outs.p, 0, 8 * (10 + size_t(kSmidSlots)), g->stream));
     DevBuf dhist(pivot ? 8 * size_t(L * L) : 8);
     if (pivot) KC_CUDA(cudaMemsetAsync(dhist.p, 0, 8 * size_t(L * L), g->stream));
 
@@ -899,6 +923,8 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
     p.visits_total = o + 5;
     p.tasks_run = o + 6;
     p.visits_per_sm = o + 8;
+    p.word_ops = o + 8 + kSmidSlots;
+    p.ext_bytes = o + 9 + kSmidSlots;
 
     cudaEvent_t e0, e1;
     KC_CUDA(cudaEventCreate(&e0));
@@ -920,8 +946,10 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
 
-    std::vector<ull> h(8 + size_t(kSmidSlots));
+    std::vector<ull> h(10 + size_t(kSmidSlots));
     KC_CUDA(cudaMemcpy(h.data(), outs.p, 8 * h.size(), cudaMemcpyDeviceToHost));
+    raw->word_ops = h[8 + kSmidSlots];
+    raw->extract_bytes = h[9 + kSmidSlots];
     for (int i = 0; i < 4; ++i) raw->limbs[i] = h[1 + i];
     raw->visits = h[5];
     raw->tasks_run = h[6];
@@ -1124,7 +1152,8 @@ namespace {
 __global__ void k_find_pivot(const uint32_t *rows, int d, const uint32_t *cand, int *out) {
     __shared__ int list[4096];
     const int W = (d + 31) >> 5;
-    int pv = warp_select_pivot(rows, W, W, cand, list);
+    ull work = 0;
+    int pv = warp_select_pivot(rows, W, W, cand, list, work);
     if (threadIdx.x == 0) out[0] = pv;
 }
 }  // namespace

@@ -111,6 +111,9 @@ void kc_do_count_bitgraph(int device, const uint64_t *rows, int64_t d, int t, in
 void kc_do_find_pivot(int device, const uint64_t *rows, int64_t d, const uint64_t *cand,
                       int64_t *pivot, uint64_t *pruned);
 
+// roofline probe (kc_probe.cu)
+void kc_do_probe(int device, double *reg_wps, double *smem_wps, double *sm_mhz);
+
 // ---------------------------------------------------------------------------
 // device helpers
 // ---------------------------------------------------------------------------

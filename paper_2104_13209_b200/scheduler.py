@@ -75,6 +75,7 @@ class CountReport:
     degeneracy: int | None = None
     load_ms: float = 0.0
     device_ms: dict | None = None  # CUDA-event times of each device phase
+    counters: dict | None = None   # this rank's kernel counters (roofline inputs)
 
     @property
     def total_ms(self):
@@ -121,6 +122,8 @@ class RawCount:
     hist: np.ndarray | None  # uint64[L, L] (pivot) or None
     visits_per_sm: np.ndarray
     count_ms: float
+    word_ops: int = 0        # roofline counters of the counting kernel
+    extract_bytes: int = 0
 
     def as_vector(self) -> np.ndarray:
         """Flatten for an element-wise u64 all-reduce."""
@@ -137,7 +140,7 @@ class RawCount:
         if self.hist is not None:
             hist = vec[6 + nsm:].reshape(self.hist.shape).copy()
         return RawCount(vec[:4].copy(), int(vec[4]), int(vec[5]), hist, vec[6:6 + nsm].copy(),
-                        self.count_ms)
+                        self.count_ms, self.word_ops, self.extract_bytes)
 
 
 def device_count_raw(og, cfg: RunConfig, task_lo: int = 0, task_hi: int = -1) -> RawCount:
@@ -159,7 +162,7 @@ def device_count_raw(og, cfg: RunConfig, task_lo: int = 0, task_hi: int = -1) ->
     used = max(nsm, int(np.flatnonzero(per_sm).max()) + 1 if per_sm.any() else 0)
     return RawCount(np.array(raw.limbs[:], dtype=np.uint64), int(raw.visits), int(raw.tasks_run),
                     None if hist is None else hist.reshape(dim, dim), per_sm[:used].copy(),
-                    float(raw.count_ms))
+                    float(raw.count_ms), int(raw.word_ops), int(raw.extract_bytes))
 
 
 def _binom_checked(n: int, r: int) -> int:
@@ -236,6 +239,7 @@ def run_count(g, cfg: RunConfig) -> CountReport:
     counts = None
     dev = {"rank": ranking.rank_ms, "orient": og.orient_ms, "count": 0.0}
     nsm = _lib.num_sms(g.device)
+    counters = None
     if cfg.k <= 2 and not cfg.all_k:
         count = g.n if cfg.k == 1 else g.m
         visits = [0] * nsm
@@ -246,8 +250,10 @@ def run_count(g, cfg: RunConfig) -> CountReport:
         visits = raw.visits_per_sm.tolist()
         dev["count"] = raw.count_ms
         sbytes = scratch_bytes(og, cfg)
+        counters = {"word_ops": raw.word_ops, "extract_bytes": raw.extract_bytes,
+                    "kernel_ms": raw.count_ms, "tasks_run": raw.tasks_run}
     count_ms = (time.perf_counter() - t1) * 1000.0
     return CountReport(n=g.n, m=g.m, d_max_undirected=g.max_degree(), d_max=og.d_max, config=cfg,
                        count=count, counts=counts, orient_ms=orient_ms, count_ms=count_ms,
                        load=load_stats(visits), scratch_bytes=sbytes,
-                       degeneracy=ranking.degeneracy, device_ms=dev)
+                       degeneracy=ranking.degeneracy, device_ms=dev, counters=counters)

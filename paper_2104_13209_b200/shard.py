@@ -85,6 +85,8 @@ def run_count_sharded(g, cfg: RunConfig, rank: int, world: int, group=None,
         ranges = balanced_ranges(task_costs(og, cfg.scheme), world)
     lo, hi = ranges[rank]
     raw = device_count_raw(og, cfg, lo, hi)
+    counters = {"word_ops": raw.word_ops, "extract_bytes": raw.extract_bytes,
+                "kernel_ms": raw.count_ms, "tasks_run": raw.tasks_run}
     if world > 1:
         raw = allreduce_raw(raw, group)
     count, counts = finalize(raw, cfg, g.n, g.m)
@@ -93,4 +95,4 @@ def run_count_sharded(g, cfg: RunConfig, rank: int, world: int, group=None,
                        count=count, counts=counts, orient_ms=orient_ms, count_ms=count_ms,
                        load=load_stats(raw.visits_per_sm.tolist()),
                        scratch_bytes=scratch_bytes(og, cfg), degeneracy=og.ranking.degeneracy,
-                       device_ms={"count": raw.count_ms})
+                       device_ms={"count": raw.count_ms}, counters=counters)
