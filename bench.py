@@ -33,7 +33,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, HERE)
 
 # BASELINE.json configs[1]: RMAT scale-18 ef16, degeneracy orientation, 1 GPU
-DEFAULTS = dict(workload="rmat18", k=7, algo="orient", scheme="vertex", criterion="degeneracy")
+DEFAULTS = dict(workload="rmat18", k=4, algo="orient", scheme="vertex", criterion="degeneracy")
 METRIC = "k-cliques/sec"
 FLUSH_BYTES = 512 << 20  # > 126 MB L2
 
@@ -336,7 +336,8 @@ def cpu_baseline(edges, a, full_count=None, target_s=12.0, workers=None):
             "sample": (f"oracle/kc_oracle.c run_tasks on tasks [0,{done_tasks}) of {n_tasks} "
                        f"({100 * frac:.3f}%), {spent:.1f}s count + {orient_s:.2f}s orient x frac"
                        + ("; full graph" if full else "")),
-            "sample_count": str(cnt), "full_count_matches": (cnt == full_count) if full else None,
+            "sample_count": str(cnt),
+            "full_count_matches": (cnt == full_count) if (full and full_count is not None) else None,
             "orient_s_full": orient_s}
 
 

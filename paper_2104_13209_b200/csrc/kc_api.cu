@@ -41,6 +41,21 @@ void require_device(int device) {
                std::string("libkc is built for sm_100a; device is ") + prop.name);
 }
 
+}  // namespace
+
+void kc_pool_setup(int device) {
+    static bool done[64] = {false};
+    if (device < 0 || device >= 64 || done[device]) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t thr = ~uint64_t(0);
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    done[device] = true;
+}
+
+namespace {
+
 kc_graph *new_graph(int device) {
     require_device(device);
     kc_graph *g = new kc_graph();
@@ -48,6 +63,7 @@ kc_graph *new_graph(int device) {
     KC_CUDA(cudaSetDevice(device));
     KC_CUDA(cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, device));
     KC_CUDA(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
+    kc_pool_setup(device);
     return g;
 }
 
@@ -57,12 +73,15 @@ void destroy(kc_graph *g) {
     cudaGetDevice(&prev);
     cudaSetDevice(g->device);
     kc_free_dag(g);
-    if (g->row_ptr) cudaFree(g->row_ptr);
-    if (g->col) cudaFree(g->col);
-    if (g->coo_src) cudaFree(g->coo_src);
-    if (g->orig_ids) cudaFree(g->orig_ids);
-    if (g->tmp) cudaFree(g->tmp);
-    if (g->stream) cudaStreamDestroy(g->stream);
+    kc_free(g->row_ptr, g->stream);
+    kc_free(g->col, g->stream);
+    kc_free(g->coo_src, g->stream);
+    kc_free(g->orig_ids, g->stream);
+    kc_free(g->tmp, g->stream);
+    if (g->stream) {
+        cudaStreamSynchronize(g->stream);
+        cudaStreamDestroy(g->stream);
+    }
     if (prev >= 0) cudaSetDevice(prev);
     delete g;
 }

@@ -28,6 +28,7 @@
 #include <vector>
 
 #include "kc_internal.cuh"
+#include "kc_traverse.cuh"
 
 namespace {
 
@@ -44,14 +45,14 @@ struct CountParams {
     int all_k;         // pivot all-k
     int dcap;          // max locals per task
     int wcap;          // ceil(dcap / 32)
-    int group_size;    // orient: 0 = auto per task
+    int group_size;    // reserved (sub-warp group size; traversal is warp-granular)
     int rows_in_smem;  // rows in shared memory, else in rows_global slot
     uint32_t *rows_global;
     int64_t rows_slot;   // u32 words per CTA slot
-    int stack_words;     // orient: smem words for group stacks
-    int pv_smem_frames;  // pivot: frames per warp held in smem
-    uint32_t *pv_global; // pivot: deep frames, per-warp slots
-    int64_t pv_slot;     // u32 words per warp slot
+    int nsm_frames;      // DFS frames per warp held in shared memory
+    int fw;              // words per frame
+    uint32_t *frames_global;  // deeper frames, one slot per warp
+    int64_t frames_slot;      // u32 words per warp slot
     int hist_dim;        // pivot: L (hist is L x L)
     ull *hist;
     int sh_hl;           // pivot: shared histogram side (len < sh_hl)
@@ -230,352 +231,90 @@ __device__ void flush_block(const CountParams &p, ull acc, ull visits, ull tasks
 }
 
 // ---------------------------------------------------------------------------
-// K5: orient traversal with sub-warp groups
+// K5: orient traversal -- warps take level-1 subtrees (kc_traverse.cuh)
 // ---------------------------------------------------------------------------
-__host__ __device__ __forceinline__ int auto_group(int W) {
-    int g = 1;
-    while (g < W && g < 32) g <<= 1;
-    return g;
-}
-
-// group stack stride in words: 2 rows (cand, rem) per frame plus a cursor
-// word per frame; stride == G (mod 32) keeps the lanes of a warp on distinct banks
-__host__ __device__ __forceinline__ int group_stride(int frames, int W, int G) {
-    int need = frames * (2 * W + 1);
-    need = (need + 31) & ~31;
-    return need + (G & 31);
-}
-
-template <int BLOCK>
-__device__ void orient_task(const CountParams &p, const uint32_t *rows, int d, uint32_t *stack,
-                            int *s_next, ull &acc, ull &visits, ull &work) {
-    const int t = p.t;
-    const int tid = threadIdx.x, lane = tid & 31;
+template <int BLOCK, int WPL>
+__device__ void orient_task(const CountParams &p, const uint32_t *rows, int d,
+                            const kct::Frames &F, int *list, int *s_next, ull &acc, ull &visits,
+                            ull &work) {
     const int W = (d + 31) >> 5, RS = row_stride(W);
-    int G = p.group_size > 0 ? p.group_size : auto_group(W);
-    const int frames = t - 2 > 0 ? t - 2 : 0;  // frames 1..t-2 are materialized
-    const int GS = group_stride(frames, W, G);
-    int NG = BLOCK / G;
-    if (frames > 0 && NG * GS > p.stack_words) NG = p.stack_words / GS;
-    const int gid = tid / G, gl = tid & (G - 1);
-    if (gid >= NG) return;
-    const int gbase = lane & ~(G - 1);
-    const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << gbase);
-    const int last = t - 2;
-    const int nchunks = (W + G - 1) / G;
-    uint32_t *st = stack + gid * GS;
-    // frame f (1..frames): cand at (f-1)*(2W+1), rem at +W, cursor at +2W
-    auto cand = [&](int f) { return st + (f - 1) * (2 * W + 1); };
-    auto rem = [&](int f) { return st + (f - 1) * (2 * W + 1) + W; };
-    auto cur = [&](int f) { return st + (f - 1) * (2 * W + 1) + 2 * W; };
-
+    const int last = p.t - 2;
+    if (last == 0) {
+        // t == 2: each local u is a visit; count popc(S0 & row u) (engine_orient.py:64-69)
+        for (int u = threadIdx.x; u < d; u += BLOCK) {
+            const uint32_t *ru = rows + u * RS;
+            int c = 0;
+            for (int w = 0; w < W; ++w) c += __popc(ru[w]);
+            acc += ull(c);
+            ++visits;
+            work += ull(W);
+        }
+        return;
+    }
+    const int lane = threadIdx.x & 31;
     for (;;) {
         int u = 0;
-        if (gl == 0) u = atomicAdd(s_next, 1);
-        u = __shfl_sync(gmask, u, 0, G);
+        if (lane == 0) u = atomicAdd(s_next, 1);
+        u = __shfl_sync(kct::FULL, u, 0);
         if (u >= d) break;
-        // frame 0 expands u (engine_orient.py:58-62); S0 = all locals
-        if (gl == 0) {
-            ++visits;
-            work += W;
-        }
-        const uint32_t *ru = rows + u * RS;
-        if (last == 0) {
-            for (int w = gl; w < W; w += G) acc += __popc(ru[w]);
-            continue;
-        }
-        uint32_t nz = 0;
-        for (int w = gl; w < W; w += G) {
-            uint32_t x = ru[w];
-            cand(1)[w] = x;
-            rem(1)[w] = x;
-            nz |= x;
-        }
-        if (!(__ballot_sync(gmask, nz != 0) & gmask)) continue;
-        int s = 1;
-        if (gl == 0) *cur(1) = 0;
-        __syncwarp(gmask);
-        while (s >= 1) {
-            int v = -1;
-            int c = *cur(s);
-            for (; c < nchunks; ++c) {
-                const int w = c * G + gl;
-                uint32_t x = w < W ? rem(s)[w] : 0u;
-                unsigned b = __ballot_sync(gmask, x != 0) & gmask;
-                if (b) {
-                    const int src = __ffs(b) - 1;
-                    const uint32_t wx = __shfl_sync(gmask, x, src);
-                    v = ((c * G + src - gbase) << 5) + __ffs(wx) - 1;
-                    if (lane == src) rem(s)[w] = x & (x - 1u);
-                    break;
-                }
-            }
-            __syncwarp(gmask);
-            if (gl == 0) *cur(s) = c;
-            __syncwarp(gmask);
-            if (v < 0) {
-                --s;
-                continue;
-            }
-            if (gl == 0) {
-                ++visits;
-                work += W;
-            }
-            const uint32_t *rv = rows + v * RS;
-            const uint32_t *cs = cand(s);
-            if (s == last) {
-                for (int w = gl; w < W; w += G) acc += __popc(cs[w] & rv[w]);
-            } else {
-                uint32_t *cn = cand(s + 1), *rn = rem(s + 1);
-                uint32_t nz2 = 0;
-                for (int w = gl; w < W; w += G) {
-                    uint32_t y = cs[w] & rv[w];
-                    cn[w] = y;
-                    rn[w] = y;
-                    nz2 |= y;
-                }
-                if (__ballot_sync(gmask, nz2 != 0) & gmask) {
-                    ++s;
-                    if (gl == 0) *cur(s) = 0;
-                    __syncwarp(gmask);
-                }
-            }
-        }
-    }
-}
-
-// ---------------------------------------------------------------------------
-// K6/K7: pivot traversal (warp groups)
-// ---------------------------------------------------------------------------
-// frame layout (words): cand[W] pruned[W] rem[W] piv npv cur
-__host__ __device__ __forceinline__ int pv_frame_words(int W) { return 3 * W + 3; }
-
-struct PivotFrames {
-    uint32_t *sm;  // first pv_smem_frames frames
-    uint32_t *gm;  // deeper frames
-    int nsm;
-    int fw;
-    __device__ __forceinline__ uint32_t *f(int s) const {
-        return s < nsm ? sm + s * fw : gm + (s - nsm) * fw;
-    }
-};
-
-// argmax_{c in cand} |cand & row(c)|, lowest c on ties (engine_pivot.py:82-101).
-// Whole warp; candidates compacted into `list`, scored lane-parallel.
-__device__ int warp_select_pivot(const uint32_t *rows, int RS, int W, const uint32_t *cand,
-                                 int *list, ull &work) {
-    const int lane = threadIdx.x & 31;
-    int n_c = 0;
-    for (int c0 = 0; c0 < W; c0 += 32) {
-        const int w = c0 + lane;
-        uint32_t x = w < W ? cand[w] : 0u;
-        int cnt = __popc(x), incl = cnt;
-        for (int o = 1; o < 32; o <<= 1) {
-            int y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += y;
-        }
-        int off = n_c + incl - cnt;
-        while (x) {
-            list[off++] = (w << 5) + __ffs(x) - 1;
-            x &= x - 1u;
-        }
-        n_c += __shfl_sync(0xffffffffu, incl, 31);
-    }
-    __syncwarp();
-    if (lane == 0) work += ull(n_c) * W;
-    ull best = 0;
-    for (int i = lane; i < n_c; i += 32) {
-        const int c = list[i];
-        const uint32_t *rc = rows + c * RS;
-        int cov = 0;
-        for (int w = 0; w < W; ++w) cov += __popc(cand[w] & rc[w]);
-        ull key = (ull(cov + 1) << 32) | ull(0xffffffffu - uint32_t(c));
-        best = key > best ? key : best;
-    }
-    for (int o = 16; o; o >>= 1) {
-        ull y = __shfl_xor_sync(0xffffffffu, best, o);
-        best = y > best ? y : best;
-    }
-    __syncwarp();
-    return int(0xffffffffu - uint32_t(best & 0xffffffffull));
-}
-
-__device__ __forceinline__ void hist_add(const CountParams &p, ull *s_hist, int len, int np) {
-    if (len < p.sh_hl) atomicAdd(&s_hist[len * (len + 1) / 2 + np], 1ull);
-    else atomicAdd(&p.hist[int64_t(len) * p.hist_dim + np], 1ull);
-}
-
-// DFS of one root branch v0 (already expanded at frame 0 into frame 1 = child)
-__device__ void pivot_dfs(const CountParams &p, const uint32_t *rows, int RS, int W,
-                          const PivotFrames &F, int *list, ull *s_hist, ull &visits,
-                          ull &work) {
-    const int lane = threadIdx.x & 31;
-    const int t = p.t;
-    const bool allk = p.all_k != 0;
-    int s = 1;
-    while (s >= 1) {
-        uint32_t *fr = F.f(s);
-        uint32_t *C = fr, *P = fr + W, *R = fr + 2 * W;
-        const int piv = int(fr[3 * W]);
-        const int npv = int(fr[3 * W + 1]);
-        int c = int(fr[3 * W + 2]);
-        int v = -1;
-        for (; c * 32 < W; ++c) {
-            const int w = c * 32 + lane;
-            uint32_t x = w < W ? R[w] : 0u;
-            unsigned b = __ballot_sync(0xffffffffu, x != 0);
-            if (b) {
-                const int src = __ffs(b) - 1;
-                const uint32_t wx = __shfl_sync(0xffffffffu, x, src);
-                v = ((c * 32 + src) << 5) + __ffs(wx) - 1;
-                if (lane == src) R[w] = x & (x - 1u);
-                break;
-            }
-        }
-        __syncwarp();
-        if (lane == 0) fr[3 * W + 2] = uint32_t(c);
-        __syncwarp();
-        if (v < 0) {
-            --s;
-            continue;
-        }
-        const int np2 = npv + (v == piv ? 1 : 0);
-        if (!allk && s + 1 - t > np2) continue;  // engine_pivot.py:152-153
         if (lane == 0) {
             ++visits;
-            work += W;
+            work += ull(W);
         }
-        const uint32_t *rv = rows + v * RS;
-        uint32_t *fn = F.f(s + 1);
-        uint32_t *Cn = fn;
-        const int vq = v >> 5;
-        const uint32_t below = (1u << (v & 31)) - 1u;
-        uint32_t nz = 0;
-        for (int w = lane; w < W; w += 32) {
-            uint32_t x = C[w] & rv[w];
-            // engine_pivot.py:158-166 drop already-branched pruned bits below v
-            if (w < vq) x &= ~P[w];
-            else if (w == vq) x &= ~(P[w] & below);
-            Cn[w] = x;
-            nz |= x;
-        }
-        const bool any = __ballot_sync(0xffffffffu, nz != 0) != 0;
-        __syncwarp();
-        if (any) {
-            const int pv = warp_select_pivot(rows, RS, W, Cn, list, work);
-            const uint32_t *rp = rows + pv * RS;
-            for (int w = lane; w < W; w += 32) {
-                uint32_t y = Cn[w] & ~rp[w];
-                fn[W + w] = y;
-                fn[2 * W + w] = y;
-            }
-            if (lane == 0) {
-                fn[3 * W] = uint32_t(pv);
-                fn[3 * W + 1] = uint32_t(np2);
-                fn[3 * W + 2] = 0u;
-            }
-            __syncwarp();
-            ++s;
-        } else if (allk || s + 1 >= t) {
-            if (lane == 0) hist_add(p, s_hist, s + 1, np2);
-        }
+        kct::orient_subtree<WPL>(rows, RS, W, last, u, F, list, acc, visits, work);
     }
 }
 
-template <int BLOCK>
-__device__ void pivot_task(const CountParams &p, const uint32_t *rows, int d, uint32_t *pv_area,
-                           int *lists, ull *s_hist, int *s_next, int *s_piv0, ull *s_key,
+// ---------------------------------------------------------------------------
+// K6/K7: pivot traversal -- root frame by the block, branches by warps
+// ---------------------------------------------------------------------------
+template <int BLOCK, int WPL>
+__device__ void pivot_task(const CountParams &p, const uint32_t *rows, int d, uint32_t *S0,
+                           uint32_t *P0, const kct::Frames &F, int *list,
+                           const kct::PivotLeafSink &sink, int *s_next, int *s_piv0, ull *s_key,
                            ull &visits, ull &work) {
     constexpr int NW = BLOCK / 32;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int W = (d + 31) >> 5, RS = row_stride(W);
-    const int t = p.t;
-    const bool allk = p.all_k != 0;
-    const int fw = pv_frame_words(W);
-    // frame 0 (shared by the block): cand = all locals, pivot by block argmax
-    uint32_t *root = pv_area;  // W words cand, W words pruned
-    for (int w = tid; w < W; w += BLOCK) {
+    // root frame (engine_pivot.py:133-136): S0 = all locals, pivot = argmax |row c|
+    for (int w = tid; w < 32 * WPL; w += BLOCK) {
         const int lo = w << 5;
-        root[w] = lo + 32 <= d ? 0xffffffffu : ((1u << (d - lo)) - 1u);
+        S0[w] = lo >= d ? 0u : (lo + 32 <= d ? kct::FULL : ((1u << (d - lo)) - 1u));
     }
     ull best = 0;
     for (int c = tid; c < d; c += BLOCK) {
         const uint32_t *rc = rows + c * RS;
         int cov = 0;
         for (int w = 0; w < W; ++w) cov += __popc(rc[w]);
-        ull key = (ull(cov + 1) << 32) | ull(0xffffffffu - uint32_t(c));
+        const ull key = (ull(cov + 1) << 32) | ull(0xffffffffu - uint32_t(c));
         best = key > best ? key : best;
     }
+#pragma unroll
     for (int o = 16; o; o >>= 1) {
-        ull y = __shfl_xor_sync(0xffffffffu, best, o);
+        const ull y = __shfl_xor_sync(kct::FULL, best, o);
         best = y > best ? y : best;
     }
     if (lane == 0) s_key[warp] = best;
-    if (tid == 0) *s_next = 0;  // next branch
     __syncthreads();
     if (tid == 0) {
         ull b = 0;
         for (int w = 0; w < NW; ++w) b = s_key[w] > b ? s_key[w] : b;
         *s_piv0 = int(0xffffffffu - uint32_t(b & 0xffffffffull));
+        work += ull(d) * W;
     }
     __syncthreads();
     const int piv0 = *s_piv0;
     const uint32_t *rp0 = rows + piv0 * RS;
-    for (int w = tid; w < W; w += BLOCK) root[W + w] = root[w] & ~rp0[w];
+    for (int w = tid; w < 32 * WPL; w += BLOCK) P0[w] = w < W ? (S0[w] & ~rp0[w]) : 0u;
     __syncthreads();
-
-    // warps take branch vertices v in pruned(0) ascending
-    PivotFrames F;
-    F.fw = fw;
-    F.nsm = p.pv_smem_frames;
-    F.sm = root + 2 * W + warp * (p.pv_smem_frames * fw);
-    F.gm = p.pv_global + (int64_t(blockIdx.x) * NW + warp) * p.pv_slot;
-    int *list = lists + warp * p.dcap;
-    const uint32_t *P0 = root + W;
     for (;;) {
         int v = 0;
         if (lane == 0) v = atomicAdd(s_next, 1);
-        v = __shfl_sync(0xffffffffu, v, 0);
+        v = __shfl_sync(kct::FULL, v, 0);
         if (v >= d) break;
         if (!((P0[v >> 5] >> (v & 31)) & 1u)) continue;
-        const int np2 = v == piv0 ? 1 : 0;
-        if (!allk && 1 - t > np2) continue;
-        if (lane == 0) {
-            ++visits;
-            work += W;
-        }
-        const uint32_t *rv = rows + v * RS;
-        uint32_t *f1 = F.f(1);
-        const int vq = v >> 5;
-        const uint32_t below = (1u << (v & 31)) - 1u;
-        uint32_t nz = 0;
-        for (int w = lane; w < W; w += 32) {
-            uint32_t x = root[w] & rv[w];
-            if (w < vq) x &= ~P0[w];
-            else if (w == vq) x &= ~(P0[w] & below);
-            f1[w] = x;
-            nz |= x;
-        }
-        const bool any = __ballot_sync(0xffffffffu, nz != 0) != 0;
-        __syncwarp();
-        if (!any) {
-            if ((allk || 1 >= t) && lane == 0) hist_add(p, s_hist, 1, np2);
-            continue;
-        }
-        const int pv = warp_select_pivot(rows, RS, W, f1, list, work);
-        const uint32_t *rp = rows + pv * RS;
-        for (int w = lane; w < W; w += 32) {
-            uint32_t y = f1[w] & ~rp[w];
-            f1[W + w] = y;
-            f1[2 * W + w] = y;
-        }
-        if (lane == 0) {
-            f1[3 * W] = uint32_t(pv);
-            f1[3 * W + 1] = uint32_t(np2);
-            f1[3 * W + 2] = 0u;
-        }
-        __syncwarp();
-        pivot_dfs(p, rows, RS, W, F, list, s_hist, visits, work);
+        kct::pivot_subtree<WPL>(rows, RS, W, p.t, p.all_k != 0, v, piv0, S0, P0, F, list, sink,
+                                visits, work);
     }
 }
 
@@ -584,26 +323,44 @@ __device__ void pivot_task(const CountParams &p, const uint32_t *rows, int d, ui
 // ---------------------------------------------------------------------------
 enum Mode { MODE_ORIENT = 0, MODE_PIVOT = 1, MODE_EXTRACT = 2 };
 
-template <int BLOCK, int MODE>
+template <int BLOCK, int MODE, int WPL>
 __global__ void __launch_bounds__(BLOCK) k_count(CountParams p) {
+    constexpr int NW = BLOCK / 32;
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ int s_next, s_piv0, s_cnt, s_task;
-    __shared__ int s_warp[BLOCK / 32];
-    __shared__ ull s_key[BLOCK / 32];
-    __shared__ ull s_red[4 * (BLOCK / 32)];
-    const int tid = threadIdx.x;
-    // layout: [hist u64][l2g i32 dcap][rows u32][work area]
-    int hist_cells = MODE == MODE_PIVOT ? p.sh_hl * (p.sh_hl + 1) / 2 : 0;
+    __shared__ int s_warp[NW];
+    __shared__ ull s_key[NW];
+    __shared__ ull s_red[4 * NW];
+    const int tid = threadIdx.x, warp = tid >> 5;
+    // layout: [hist u64][l2g i32 dcap][rows u32][S0 P0][per warp: list dcap, frames]
+    const int hist_cells = MODE == MODE_PIVOT ? p.sh_hl * (p.sh_hl + 1) / 2 : 0;
     ull *s_hist = reinterpret_cast<ull *>(smem);
     int32_t *l2g = reinterpret_cast<int32_t *>(smem + 8 * hist_cells);
-    uint32_t *area = reinterpret_cast<uint32_t *>(l2g + p.dcap);
+    uint32_t *area = reinterpret_cast<uint32_t *>(l2g + ((p.dcap + 3) & ~3));
     uint32_t *rows;
     if (p.rows_in_smem) {
         rows = area;
-        area += int64_t(p.dcap) * row_stride(p.wcap);
+        area += ((int64_t(p.dcap) * row_stride(p.wcap) + 3) & ~3);
     } else {
         rows = p.rows_global + int64_t(blockIdx.x) * p.rows_slot;
     }
+    int32_t *scratch = reinterpret_cast<int32_t *>(area);  // edge-scheme staging (pre-traversal)
+    uint32_t *S0 = area, *P0 = area + 32 * WPL;
+    if (MODE == MODE_PIVOT) area += 64 * WPL;
+    const int per_warp = ((p.dcap + 3) & ~3) + p.nsm_frames * p.fw;
+    int *list = reinterpret_cast<int *>(area + warp * per_warp);
+    kct::Frames F;
+    F.sm = area + warp * per_warp + ((p.dcap + 3) & ~3);
+    F.nsm = p.nsm_frames;
+    F.fw = p.fw;
+    F.gm = p.frames_global ? p.frames_global + (int64_t(blockIdx.x) * NW + warp) * p.frames_slot
+                           : nullptr;
+    kct::PivotLeafSink sink;
+    sink.s_hist = s_hist;
+    sink.sh_hl = p.sh_hl;
+    sink.g_hist = p.hist;
+    sink.L = p.hist_dim;
+
     for (int i = tid; i < hist_cells; i += BLOCK) s_hist[i] = 0;
     ull acc = 0, visits = 0, tasks = 0, work = 0, bytes = 0;
     const bool directed = MODE == MODE_ORIENT || (MODE == MODE_EXTRACT && p.directed_out);
@@ -623,10 +380,9 @@ __global__ void __launch_bounds__(BLOCK) k_count(CountParams p) {
             d = load_given<BLOCK>(p, rows);
         } else {
             const int32_t task = p.tasks[s_task];
-            // int32 scratch for the edge scheme lives in the work area
             const bool need_rows = MODE == MODE_EXTRACT || MODE == MODE_PIVOT || t >= 2;
-            d = build_task<BLOCK>(p, task, l2g, rows, reinterpret_cast<int32_t *>(area), need_rows,
-                                  directed, &s_cnt, s_warp, bytes);
+            d = build_task<BLOCK>(p, task, l2g, rows, scratch, need_rows, directed, &s_cnt, s_warp,
+                                  bytes);
         }
         if (MODE == MODE_EXTRACT) {
             const int W = (d + 31) >> 5, RS = row_stride(W);
@@ -650,12 +406,10 @@ __global__ void __launch_bounds__(BLOCK) k_count(CountParams p) {
             continue;
         }
         if (MODE == MODE_ORIENT) {
-            orient_task<BLOCK>(p, rows, d, area, &s_next, acc, visits, work);
+            orient_task<BLOCK, WPL>(p, rows, d, F, list, &s_next, acc, visits, work);
         } else {
-            pivot_task<BLOCK>(p, rows, d, area, reinterpret_cast<int *>(
-                                  area + 2 * ((d + 31) >> 5) +
-                                  (BLOCK / 32) * p.pv_smem_frames * pv_frame_words((d + 31) >> 5)),
-                              s_hist, &s_next, &s_piv0, s_key, visits, work);
+            pivot_task<BLOCK, WPL>(p, rows, d, S0, P0, F, list, sink, &s_next, &s_piv0, s_key,
+                                   visits, work);
         }
     }
     __syncthreads();
@@ -722,13 +476,20 @@ inline int grid_1d(int64_t n, int sms) {
     return int(b < 1 ? 1 : b);
 }
 
+// stream of the current library call: DevBuf allocations are stream-ordered on it
+thread_local cudaStream_t tl_stream = nullptr;
+struct StreamScope {
+    cudaStream_t prev;
+    explicit StreamScope(cudaStream_t s) : prev(tl_stream) { tl_stream = s; }
+    ~StreamScope() { tl_stream = prev; }
+};
+
 struct DevBuf {
     void *p = nullptr;
+    cudaStream_t s = nullptr;
     DevBuf() = default;
-    explicit DevBuf(size_t bytes) { p = kc_alloc<uint8_t>(bytes); }
-    ~DevBuf() {
-        if (p) cudaFree(p);
-    }
+    explicit DevBuf(size_t bytes) : s(tl_stream) { p = kc_alloc<uint8_t>(bytes, s); }
+    ~DevBuf() { kc_free(p, s); }
     template <typename T>
     T *as() const {
         return reinterpret_cast<T *>(p);
@@ -793,47 +554,44 @@ int64_t build_tasks(kc_graph *g, int scheme, int64_t lo, int64_t hi, int min_d, 
     return n_sel;
 }
 
-constexpr int kBlock = 256;
+constexpr int kBlock = 128;
 constexpr int kSmidSlots = 1024;  // %smid can exceed the SM count
 constexpr int kSmemMax = 220 * 1024;
+constexpr int kSmemTarget = 100 * 1024;  // aim for >= 2 resident CTAs per SM
 
-struct Plan {
-    size_t smem = 0;
-    int blocks = 0;
-};
-
-size_t orient_stack_words(int t, int wcap, int group_size) {
-    const int frames = t - 2 > 0 ? t - 2 : 0;
-    if (frames == 0) return 32;
-    size_t best = 0;
-    for (int W = 1; W <= wcap; ++W) {
-        int G = group_size > 0 ? group_size : auto_group(W);
-        size_t need = size_t(kBlock / G) * group_stride(frames, W, G);
-        best = need > best ? need : best;
-    }
-    return best;
+// DFS frames a warp can touch: orient frames 1..t-3 (frame t-2 is scored in
+// registers), pivot frames 1..d (+1 guard)
+int frames_needed(int mode, int t, int dcap) {
+    if (mode == MODE_ORIENT) return std::max(1, std::min(t - 2, dcap + 1));
+    return dcap + 2;
 }
 
-template <int MODE>
-void launch(kc_graph *g, CountParams &p, int grid_override = 0) {
-    const int NW = kBlock / 32;
-    size_t hist_bytes = MODE == MODE_PIVOT ? 8 * size_t(p.sh_hl) * (p.sh_hl + 1) / 2 : 0;
-    size_t l2g_bytes = 4 * size_t(p.dcap > 0 ? p.dcap : 1);
-    size_t rows_words = size_t(p.dcap) * row_stride(p.wcap);
-    size_t work_words = 0;
-    if (MODE == MODE_ORIENT) {
-        work_words = orient_stack_words(p.t, p.wcap, p.group_size);
-    } else if (MODE == MODE_PIVOT) {
-        const int fw = pv_frame_words(p.wcap);
-        // root (2W) + per-warp frames + per-warp candidate lists
-        work_words = 2 * p.wcap + size_t(NW) * p.pv_smem_frames * fw + size_t(NW) * p.dcap;
-    }
-    if (p.scheme == KC_SCHEME_EDGE) work_words = std::max(work_words, size_t(p.dcap));
-    size_t base = hist_bytes + l2g_bytes + 4 * work_words + 64;
-    p.rows_in_smem = base + 4 * rows_words <= size_t(kSmemMax);
-    size_t smem = base + (p.rows_in_smem ? 4 * rows_words : 0);
+template <int MODE, int WPL>
+void launch_wpl(kc_graph *g, CountParams &p, int grid_override) {
+    constexpr int NW = kBlock / 32;
+    const size_t hist_bytes = MODE == MODE_PIVOT ? 8 * size_t(p.sh_hl) * (p.sh_hl + 1) / 2 : 0;
+    const size_t dpad = size_t((p.dcap + 3) & ~3);
+    const size_t l2g_bytes = 4 * dpad;
+    const size_t rows_words = (size_t(p.dcap) * row_stride(p.wcap) + 3) & ~size_t(3);
+    p.fw = MODE == MODE_PIVOT ? 64 * WPL + 4 : 32 * WPL + 4;
+    const int need = frames_needed(MODE, p.t, p.dcap);
+    auto area_words = [&](int nsm) {
+        size_t w = (MODE == MODE_PIVOT ? 64 * WPL : 0) + size_t(NW) * (dpad + size_t(nsm) * p.fw);
+        if (p.scheme == KC_SCHEME_EDGE) w = std::max(w, dpad);
+        return w;
+    };
+    // as many shared frames as fit the target budget (at least 4, at most need)
+    int nsm = std::min(need, 64);
+    auto total = [&](int ns, bool rows_smem) {
+        return hist_bytes + l2g_bytes + 4 * area_words(ns) + (rows_smem ? 4 * rows_words : 0) + 64;
+    };
+    p.rows_in_smem = total(std::min(nsm, 4), true) <= size_t(kSmemMax);
+    while (nsm > 4 && total(nsm, p.rows_in_smem) > size_t(kSmemTarget)) nsm >>= 1;
+    while (nsm > 1 && total(nsm, p.rows_in_smem) > size_t(kSmemMax)) --nsm;
+    p.nsm_frames = nsm;
+    const size_t smem = total(nsm, p.rows_in_smem);
     KC_REQUIRE(smem <= size_t(kSmemMax), KC_ENOMEM, "per-task scratch exceeds shared memory");
-    auto kern = k_count<kBlock, MODE>;
+    auto kern = k_count<kBlock, MODE, WPL>;
     KC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     int per_sm = 0;
     KC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBlock, smem));
@@ -841,23 +599,32 @@ void launch(kc_graph *g, CountParams &p, int grid_override = 0) {
     int grid = grid_override > 0 ? grid_override : per_sm * g->num_sms;
     if (p.n_tasks > 0 && int64_t(grid) > p.n_tasks && !grid_override) grid = int(p.n_tasks);
     if (grid < 1) grid = 1;
-    DevBuf rows_g, pv_g;
+    DevBuf rows_g, fr_g;
     if (!p.rows_in_smem) {
         p.rows_slot = int64_t(rows_words);
         new (&rows_g) DevBuf(4 * rows_words * size_t(grid));
         p.rows_global = rows_g.as<uint32_t>();
     }
-    if (MODE == MODE_PIVOT) {
-        const int fw = pv_frame_words(p.wcap);
-        int64_t deep = int64_t(p.dcap) + 2 - p.pv_smem_frames;
-        if (deep < 1) deep = 1;
-        p.pv_slot = deep * fw;
-        new (&pv_g) DevBuf(4 * size_t(p.pv_slot) * size_t(grid) * NW);
-        p.pv_global = pv_g.as<uint32_t>();
+    p.frames_global = nullptr;
+    p.frames_slot = 0;
+    if (MODE != MODE_EXTRACT && need > nsm) {
+        p.frames_slot = int64_t(need - nsm) * p.fw;
+        new (&fr_g) DevBuf(4 * size_t(p.frames_slot) * size_t(grid) * NW);
+        p.frames_global = fr_g.as<uint32_t>();
     }
     kern<<<grid, kBlock, smem, g->stream>>>(p);
     KC_CUDA(cudaGetLastError());
     KC_CUDA(cudaStreamSynchronize(g->stream));
+}
+
+template <int MODE>
+void launch(kc_graph *g, CountParams &p, int grid_override = 0) {
+    const int wpl = (p.wcap + 31) / 32;
+    KC_REQUIRE(wpl <= 4, KC_EINVAL,
+               "oriented max out-degree above 4096 locals is not supported by the bitmap engine");
+    if (MODE == MODE_EXTRACT || wpl <= 1) launch_wpl<MODE, 1>(g, p, grid_override);
+    else if (wpl == 2) launch_wpl<MODE, 2>(g, p, grid_override);
+    else launch_wpl<MODE, 4>(g, p, grid_override);
 }
 
 }  // namespace
@@ -887,6 +654,7 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
     }
     if (visits_per_sm) memset(visits_per_sm, 0, sizeof(uint64_t) * size_t(n_sm));
     kc_device_guard guard(g->device);
+    StreamScope scope(g->stream);
 
     int64_t all = kc_task_count(g, a->scheme);
     int64_t lo = a->task_lo < 0 ? 0 : a->task_lo;
@@ -932,10 +700,8 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
     KC_CUDA(cudaEventRecord(e0, g->stream));
     if (n_tasks > 0) {
         if (pivot) {
-            p.pv_smem_frames = 8;
             launch<MODE_PIVOT>(g, p);
         } else {
-            p.stack_words = int(orient_stack_words(t, p.wcap, gs));
             launch<MODE_ORIENT>(g, p);
         }
     }
@@ -947,7 +713,11 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
     cudaEventDestroy(e1);
 
     std::vector<ull> h(10 + size_t(kSmidSlots));
-    KC_CUDA(cudaMemcpy(h.data(), outs.p, 8 * h.size(), cudaMemcpyDeviceToHost));
+    KC_CUDA(cudaMemcpyAsync(h.data(), outs.p, 8 * h.size(), cudaMemcpyDeviceToHost, g->stream));
+    if (pivot)
+        KC_CUDA(cudaMemcpyAsync(hist, dhist.p, 8 * size_t(L * L), cudaMemcpyDeviceToHost,
+                                g->stream));
+    KC_CUDA(cudaStreamSynchronize(g->stream));
     raw->word_ops = h[8 + kSmidSlots];
     raw->extract_bytes = h[9 + kSmidSlots];
     for (int i = 0; i < 4; ++i) raw->limbs[i] = h[1 + i];
@@ -956,7 +726,6 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
     raw->count_ms = ms;
     if (visits_per_sm)
         for (int i = 0; i < n_sm && i < kSmidSlots; ++i) visits_per_sm[i] = h[8 + i];
-    if (pivot) KC_CUDA(cudaMemcpy(hist, dhist.p, 8 * size_t(L * L), cudaMemcpyDeviceToHost));
 }
 
 void kc_do_extract(kc_graph *g, int scheme, int64_t task, int directed, int64_t *l2g,
@@ -965,12 +734,13 @@ void kc_do_extract(kc_graph *g, int scheme, int64_t task, int directed, int64_t 
     const int64_t N = scheme == KC_SCHEME_EDGE ? g->m_dir : g->n;
     KC_REQUIRE(task >= 0 && task < N, KC_EINVAL, "task out of range");
     kc_device_guard guard(g->device);
+    StreamScope scope(g->stream);
     const int dcap = int(std::max<int64_t>(g->d_max, 1));
     const int wcap = (dcap + 31) / 32;
     DevBuf tk(4), rows(4 * size_t(dcap) * wcap), l(4 * size_t(dcap)), dd(4), outs(64);
     int32_t t32 = int32_t(task);
-    KC_CUDA(cudaMemcpy(tk.p, &t32, 4, cudaMemcpyHostToDevice));
-    KC_CUDA(cudaMemset(outs.p, 0, 64));
+    KC_CUDA(cudaMemcpyAsync(tk.p, &t32, 4, cudaMemcpyHostToDevice, g->stream));
+    KC_CUDA(cudaMemsetAsync(outs.p, 0, 64, g->stream));
     CountParams p;
     memset(&p, 0, sizeof(p));
     p.orow = g->orow_ptr;
@@ -989,7 +759,8 @@ void kc_do_extract(kc_graph *g, int scheme, int64_t task, int directed, int64_t 
     p.task_counter = outs.as<ull>();
     launch<MODE_EXTRACT>(g, p, 1);
     int d = 0;
-    KC_CUDA(cudaMemcpy(&d, dd.p, 4, cudaMemcpyDeviceToHost));
+    KC_CUDA(cudaMemcpyAsync(&d, dd.p, 4, cudaMemcpyDeviceToHost, g->stream));
+    KC_CUDA(cudaStreamSynchronize(g->stream));
     KC_REQUIRE(d <= cap, KC_EINVAL, "scratch BitGraph too small for this task");
     const int W = (d + 31) / 32;
     const int64_t wpr = (d + 63) / 64;
@@ -997,8 +768,10 @@ void kc_do_extract(kc_graph *g, int scheme, int64_t task, int directed, int64_t 
     std::vector<int32_t> hl(d > 0 ? d : 1);
     std::vector<uint32_t> hr(size_t(d) * W + 1);
     if (d) {
-        KC_CUDA(cudaMemcpy(hl.data(), l.p, 4 * size_t(d), cudaMemcpyDeviceToHost));
-        KC_CUDA(cudaMemcpy(hr.data(), rows.p, 4 * size_t(d) * W, cudaMemcpyDeviceToHost));
+        KC_CUDA(cudaMemcpyAsync(hl.data(), l.p, 4 * size_t(d), cudaMemcpyDeviceToHost, g->stream));
+        KC_CUDA(cudaMemcpyAsync(hr.data(), rows.p, 4 * size_t(d) * W, cudaMemcpyDeviceToHost,
+                                g->stream));
+        KC_CUDA(cudaStreamSynchronize(g->stream));
     }
     for (int i = 0; i < d; ++i) {
         l2g[i] = hl[i];
@@ -1033,7 +806,8 @@ void kc_do_count_bitgraph(int device, const uint64_t *rows64, int64_t d64, int t
     kc_graph tmpg;
     tmpg.device = device;
     KC_CUDA(cudaDeviceGetAttribute(&tmpg.num_sms, cudaDevAttrMultiProcessorCount, device));
-    KC_CUDA(cudaStreamCreateWithFlags(&tmpg.stream, cudaStreamNonBlocking));
+    tmpg.stream = nullptr;  // legacy stream: host copies below are ordered with it
+    StreamScope scope(nullptr);
     const int W = (d + 31) / 32;
     const int64_t wpr = (d + 63) / 64;
     std::vector<uint32_t> r32(size_t(d) * W);
@@ -1069,19 +843,15 @@ void kc_do_count_bitgraph(int device, const uint64_t *rows64, int64_t d64, int t
     p.visits_per_sm = o + 8;
     try {
         if (pivot) {
-            p.pv_smem_frames = 8;
             launch<MODE_PIVOT>(&tmpg, p, 1);
         } else {
-            p.stack_words = int(orient_stack_words(t, W, 0));
             launch<MODE_ORIENT>(&tmpg, p, 1);
         }
     } catch (...) {
-        cudaStreamDestroy(tmpg.stream);
         throw;
     }
     std::vector<ull> h(8);
     KC_CUDA(cudaMemcpy(h.data(), outs.p, 64, cudaMemcpyDeviceToHost));
-    cudaStreamDestroy(tmpg.stream);
     typedef unsigned __int128 u128;
     if (!pivot) {
         u128 c = u128(h[1]) + (u128(h[2]) << 32);
@@ -1149,11 +919,15 @@ void kc_do_count_bitgraph(int device, const uint64_t *rows64, int64_t d64, int t
 }
 
 namespace {
+template <int WPL>
 __global__ void k_find_pivot(const uint32_t *rows, int d, const uint32_t *cand, int *out) {
     __shared__ int list[4096];
-    const int W = (d + 31) >> 5;
+    const int W = (d + 31) >> 5, lane = threadIdx.x & 31;
+    kct::Set<WPL> C;
+#pragma unroll
+    for (int p = 0; p < WPL; ++p) C.w[p] = p * 32 + lane < W ? cand[p * 32 + lane] : 0u;
     ull work = 0;
-    int pv = warp_select_pivot(rows, W, W, cand, list, work);
+    const int pv = kct::select_pivot<WPL>(rows, W, C, list, lane, work, W);
     if (threadIdx.x == 0) out[0] = pv;
 }
 }  // namespace
@@ -1168,6 +942,7 @@ void kc_do_find_pivot(int device, const uint64_t *rows64, int64_t d64, const uin
     for (int64_t w = 0; w < wpr; ++w) any |= cand64[w] != 0;
     KC_REQUIRE(any, KC_EINVAL, "candidate set is empty");
     kc_device_guard guard(device);
+    StreamScope scope(nullptr);
     std::vector<uint32_t> r32(size_t(d) * W), c32(W);
     for (int i = 0; i < d; ++i)
         for (int w = 0; w < W; ++w) {
@@ -1178,7 +953,9 @@ void kc_do_find_pivot(int device, const uint64_t *rows64, int64_t d64, const uin
     DevBuf dr(4 * r32.size()), dc(4 * size_t(W)), dout(4);
     KC_CUDA(cudaMemcpy(dr.p, r32.data(), 4 * r32.size(), cudaMemcpyHostToDevice));
     KC_CUDA(cudaMemcpy(dc.p, c32.data(), 4 * c32.size(), cudaMemcpyHostToDevice));
-    k_find_pivot<<<1, 32>>>(dr.as<uint32_t>(), d, dc.as<uint32_t>(), dout.as<int>());
+    if (W <= 32) k_find_pivot<1><<<1, 32>>>(dr.as<uint32_t>(), d, dc.as<uint32_t>(), dout.as<int>());
+    else if (W <= 64) k_find_pivot<2><<<1, 32>>>(dr.as<uint32_t>(), d, dc.as<uint32_t>(), dout.as<int>());
+    else k_find_pivot<4><<<1, 32>>>(dr.as<uint32_t>(), d, dc.as<uint32_t>(), dout.as<int>());
     KC_CUDA(cudaGetLastError());
     int pv = 0;
     KC_CUDA(cudaMemcpy(&pv, dout.p, 4, cudaMemcpyDeviceToHost));

@@ -14,12 +14,15 @@
 //
 // All kernels are memory-bound integer passes: grid-stride loops, coalesced
 // int32/int64 streams, no shared-memory staging needed.
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
 #include <algorithm>
 #include <vector>
 
 #include "kc_internal.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace {
 
@@ -140,65 +143,86 @@ __global__ void k_orient_flags(const int32_t *__restrict__ col, const int32_t *_
 }
 
 // ---- K3 ------------------------------------------------------------------
-__global__ void k_peel_init(const int64_t *__restrict__ row_ptr, int64_t n,
-                            int32_t *__restrict__ deg, int32_t *__restrict__ round_of) {
-    for (int64_t v = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; v < n;
-         v += int64_t(gridDim.x) * blockDim.x) {
+// K3 as ONE persistent cooperative kernel: the whole bulk-synchronous peel
+// runs on the device with grid-wide barriers (no host round trip per round).
+// order[] receives vertices in removal order; round r's frontier is the slice
+// [head, end) of it, and relax appends the next round's frontier at the tail.
+// ctl: [0] tail, [1]/[2] min live degree (alternating per scan), [3] degeneracy,
+//      [4] rounds.
+__global__ void k_peel_coop(const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
+                            int64_t n, int32_t *__restrict__ deg, int32_t *__restrict__ round_of,
+                            int32_t *__restrict__ order, int32_t *ctl) {
+    cg::grid_group grid = cg::this_grid();
+    const int64_t gtid = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+    const int64_t gsz = int64_t(gridDim.x) * blockDim.x;
+    const int lane = threadIdx.x & 31;
+    const int64_t gwarp = gtid >> 5, nwarps = gsz >> 5;
+    const int32_t BIG = 0x7fffffff;
+    for (int64_t v = gtid; v < n; v += gsz) {
         deg[v] = int32_t(row_ptr[v + 1] - row_ptr[v]);
         round_of[v] = -1;
     }
-}
-
-// live vertices with residual degree <= level start a level; also the
-// minimum live degree for the next level.  Warp-aggregated atomics.
-__global__ void k_peel_scan(const int32_t *__restrict__ deg, const int32_t *__restrict__ round_of,
-                            int64_t n, int32_t level, int32_t *__restrict__ frontier,
-                            int32_t *__restrict__ counters /* [0]=size [1]=min deg */) {
-    const int lane = threadIdx.x & 31;
-    for (int64_t base = blockIdx.x * int64_t(blockDim.x); base < n;
-         base += int64_t(gridDim.x) * blockDim.x) {
-        int64_t v = base + threadIdx.x;
-        bool live = v < n && round_of[v] < 0;
-        int32_t d = live ? deg[v] : 0x7fffffff;
-        bool take = live && d <= level;
-        unsigned mask = __ballot_sync(0xffffffffu, take);
-        int off = 0;
-        if (lane == 0 && mask) off = atomicAdd(&counters[0], __popc(mask));
-        off = __shfl_sync(0xffffffffu, off, 0);
-        if (take) frontier[off + __popc(mask & ((1u << lane) - 1))] = int32_t(v);
-        int32_t dm = (live && !take) ? d : 0x7fffffff;
-        for (int o = 16; o; o >>= 1) dm = min(dm, __shfl_xor_sync(0xffffffffu, dm, o));
-        if (lane == 0 && dm != 0x7fffffff) atomicMin(&counters[1], dm);
+    if (gtid == 0) {
+        ctl[0] = 0;
+        ctl[1] = BIG;
+        ctl[2] = BIG;
     }
-}
-
-__global__ void k_peel_mark(const int32_t *__restrict__ frontier, const int32_t *__restrict__ size,
-                            int32_t round, int32_t *__restrict__ round_of) {
-    int32_t cnt = *size;
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < cnt;
-         i += int64_t(gridDim.x) * blockDim.x)
-        round_of[frontier[i]] = round;
-}
-
-// warp per frontier vertex: decrement live neighbours; a neighbour that
-// crosses level+1 -> level joins the next frontier
-__global__ void k_peel_relax(const int32_t *__restrict__ frontier, const int32_t *__restrict__ size,
-                             const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
-                             int32_t level, int32_t *__restrict__ deg,
-                             const int32_t *__restrict__ round_of, int32_t *__restrict__ next,
-                             int32_t *__restrict__ next_size) {
-    int32_t cnt = *size;
-    int lane = threadIdx.x & 31;
-    int64_t warp = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
-    int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
-    for (int64_t i = warp; i < cnt; i += nwarps) {
-        int32_t v = frontier[i];
-        for (int64_t e = row_ptr[v] + lane; e < row_ptr[v + 1]; e += 32) {
-            int32_t w = col[e];
-            if (round_of[w] >= 0) continue;
-            int32_t old = atomicSub(&deg[w], 1);
-            if (old == level + 1) next[atomicAdd(next_size, 1)] = w;  // rare: one per crossing
+    grid.sync();
+    volatile int32_t *vctl = ctl;
+    int64_t head = 0;
+    int32_t level = 0, round = 0, degen = 0;
+    int scans = 0;
+    while (head < n) {
+        // scan: live vertices of residual degree <= level start a level
+        const int mslot = 1 + (scans & 1);
+        for (int64_t base = gtid - lane; base < n; base += gsz) {
+            const int64_t v = base + lane;
+            const bool live = v < n && round_of[v] < 0;
+            const int32_t d = live ? deg[v] : BIG;
+            const bool take = live && d <= level;
+            const unsigned mask = __ballot_sync(0xffffffffu, take);
+            int off = 0;
+            if (lane == 0 && mask) off = atomicAdd(&ctl[0], __popc(mask));
+            off = __shfl_sync(0xffffffffu, off, 0);
+            if (take) order[off + __popc(mask & ((1u << lane) - 1))] = int32_t(v);
+            int32_t dm = (live && !take) ? d : BIG;
+            for (int o = 16; o; o >>= 1) dm = min(dm, __shfl_xor_sync(0xffffffffu, dm, o));
+            if (lane == 0 && dm != BIG) atomicMin(&ctl[mslot], dm);
         }
+        // the other min slot was last read before the previous barrier
+        if (gtid == 0) ctl[1 + ((scans + 1) & 1)] = BIG;
+        grid.sync();
+        int64_t end = vctl[0];
+        const int32_t mn = vctl[mslot];
+        ++scans;
+        if (end == head) {
+            level = mn;  // no live vertex at this level: jump to the next one
+            continue;
+        }
+        degen = level > degen ? level : degen;
+        while (end > head) {
+            for (int64_t i = head + gtid; i < end; i += gsz) round_of[order[i]] = round;
+            grid.sync();
+            // warp per frontier vertex: decrement live neighbours; one that
+            // crosses level+1 -> level joins the next round's frontier
+            for (int64_t i = head + gwarp; i < end; i += nwarps) {
+                const int32_t v = order[i];
+                for (int64_t e = row_ptr[v] + lane; e < row_ptr[v + 1]; e += 32) {
+                    const int32_t w = col[e];
+                    if (round_of[w] >= 0) continue;
+                    const int32_t old = atomicSub(&deg[w], 1);
+                    if (old == level + 1) order[atomicAdd(&ctl[0], 1)] = w;
+                }
+            }
+            grid.sync();
+            head = end;
+            end = vctl[0];
+            ++round;
+        }
+    }
+    if (gtid == 0) {
+        ctl[3] = degen;
+        ctl[4] = round;
     }
 }
 
@@ -239,11 +263,11 @@ __global__ void k_vertex_task_flags(const int64_t *__restrict__ orow, int64_t n,
 // ---------------------------------------------------------------------------
 void *kc_tmp(kc_graph *g, size_t bytes) {
     if (bytes > g->tmp_bytes) {
-        if (g->tmp) KC_CUDA(cudaFree(g->tmp));
+        if (g->tmp) kc_free(g->tmp, g->stream);
         g->tmp = nullptr;
         g->tmp_bytes = 0;
         size_t want = bytes + bytes / 4 + 1024;
-        g->tmp = kc_alloc<uint8_t>(want);
+        g->tmp = kc_alloc<uint8_t>(want, g->stream);
         g->tmp_bytes = want;
     }
     return g->tmp;
@@ -265,7 +289,7 @@ static void sort_u64(kc_graph *g, uint64_t *keys_in, uint64_t *keys_out, int64_t
 }
 
 static void finish_csr_stats(kc_graph *g) {
-    unsigned long long *d_max = kc_alloc<unsigned long long>(1);
+    unsigned long long *d_max = kc_alloc<unsigned long long>(1, g->stream);
     KC_CUDA(cudaMemsetAsync(d_max, 0, 8, g->stream));
     if (g->n)
         k_degree_stats<<<grid_for(g->n, g->num_sms), kThreads, 0, g->stream>>>(g->row_ptr, g->n,
@@ -273,7 +297,7 @@ static void finish_csr_stats(kc_graph *g) {
     unsigned long long h = 0;
     KC_CUDA(cudaMemcpyAsync(&h, d_max, 8, cudaMemcpyDeviceToHost, g->stream));
     KC_CUDA(cudaStreamSynchronize(g->stream));
-    cudaFree(d_max);
+    kc_free(d_max, g->stream);
     g->d_max_und = int64_t(h);
 }
 
@@ -283,8 +307,8 @@ void kc_build_from_edges(kc_graph *g, const int64_t *pairs, int64_t m, const int
     EventTimer timer(g->stream);
     int64_t tot = 2 * m + n_extra;
     // ids = union1d(pairs.ravel(), extra)          graph.py:177-181
-    int64_t *d_all = kc_alloc<int64_t>(tot);
-    int64_t *d_sorted = kc_alloc<int64_t>(tot);
+    int64_t *d_all = kc_alloc<int64_t>(tot, g->stream);
+    int64_t *d_sorted = kc_alloc<int64_t>(tot, g->stream);
     if (m) KC_CUDA(cudaMemcpyAsync(d_all, pairs, 16 * m, cudaMemcpyHostToDevice, g->stream));
     if (n_extra)
         KC_CUDA(cudaMemcpyAsync(d_all + 2 * m, extra, 8 * n_extra, cudaMemcpyHostToDevice,
@@ -298,7 +322,7 @@ void kc_build_from_edges(kc_graph *g, const int64_t *pairs, int64_t m, const int
         void *tmp = kc_tmp(g, bytes);
         KC_CUDA(cub::DeviceRadixSort::SortKeys(tmp, bytes, d_all, d_sorted, int(tot), 0, 64,
                                                g->stream));
-        int32_t *d_n = kc_alloc<int32_t>(1);
+        int32_t *d_n = kc_alloc<int32_t>(1, g->stream);
         bytes = 0;
         KC_CUDA(cub::DeviceSelect::Unique(nullptr, bytes, d_sorted, d_all, d_n, int(tot),
                                           g->stream));
@@ -307,30 +331,30 @@ void kc_build_from_edges(kc_graph *g, const int64_t *pairs, int64_t m, const int
         int32_t hn = 0;
         KC_CUDA(cudaMemcpyAsync(&hn, d_n, 4, cudaMemcpyDeviceToHost, g->stream));
         KC_CUDA(cudaStreamSynchronize(g->stream));
-        cudaFree(d_n);
+        kc_free(d_n, g->stream);
         n = hn;
     }
-    cudaFree(d_sorted);
+    kc_free(d_sorted, g->stream);
     g->n = n;
     g->m = n ? m : 0;
-    g->orig_ids = kc_alloc<int64_t>(n);
+    g->orig_ids = kc_alloc<int64_t>(n, g->stream);
     if (n)
         KC_CUDA(cudaMemcpyAsync(g->orig_ids, d_all, 8 * n, cudaMemcpyDeviceToDevice, g->stream));
-    g->row_ptr = kc_alloc<int64_t>(n + 1);
-    g->col = kc_alloc<int32_t>(2 * g->m);
-    g->coo_src = kc_alloc<int32_t>(2 * g->m);
+    g->row_ptr = kc_alloc<int64_t>(n + 1, g->stream);
+    g->col = kc_alloc<int32_t>(2 * g->m, g->stream);
+    g->coo_src = kc_alloc<int32_t>(2 * g->m, g->stream);
     if (n == 0) {
         KC_CUDA(cudaMemsetAsync(g->row_ptr, 0, 8, g->stream));
     } else if (g->m == 0) {
         KC_CUDA(cudaMemsetAsync(g->row_ptr, 0, 8 * (n + 1), g->stream));
     } else {
         // raw pairs again (d_all now holds the ids); reuse a fresh buffer
-        int64_t *d_pairs = kc_alloc<int64_t>(2 * m);
+        int64_t *d_pairs = kc_alloc<int64_t>(2 * m, g->stream);
         KC_CUDA(cudaMemcpyAsync(d_pairs, pairs, 16 * m, cudaMemcpyHostToDevice, g->stream));
         int bits = kc_bits_for(n - 1 > 0 ? n - 1 : 1);
         KC_REQUIRE(2 * bits <= 64 && n < (int64_t(1) << 31), KC_EINVAL, "too many vertices");
-        uint64_t *keys = kc_alloc<uint64_t>(2 * m);
-        uint64_t *keys2 = kc_alloc<uint64_t>(2 * m);
+        uint64_t *keys = kc_alloc<uint64_t>(2 * m, g->stream);
+        uint64_t *keys2 = kc_alloc<uint64_t>(2 * m, g->stream);
         k_pack_pairs<<<grid_for(m, g->num_sms), kThreads, 0, g->stream>>>(d_pairs, m, g->orig_ids,
                                                                            n, bits, keys);
         KC_CUDA(cudaGetLastError());
@@ -343,11 +367,11 @@ void kc_build_from_edges(kc_graph *g, const int64_t *pairs, int64_t m, const int
                                                                             g->row_ptr);
         KC_CUDA(cudaGetLastError());
         KC_CUDA(cudaStreamSynchronize(g->stream));
-        cudaFree(keys);
-        cudaFree(keys2);
-        cudaFree(d_pairs);
+        kc_free(keys, g->stream);
+        kc_free(keys2, g->stream);
+        kc_free(d_pairs, g->stream);
     }
-    cudaFree(d_all);
+    kc_free(d_all, g->stream);
     g->build_ms = timer.stop();
     finish_csr_stats(g);
 }
@@ -358,10 +382,10 @@ void kc_build_from_csr(kc_graph *g, int64_t n, int64_t m, const int64_t *row_ptr
     EventTimer timer(g->stream);
     g->n = n;
     g->m = m;
-    g->row_ptr = kc_alloc<int64_t>(n + 1);
-    g->col = kc_alloc<int32_t>(2 * m);
-    g->coo_src = kc_alloc<int32_t>(2 * m);
-    g->orig_ids = kc_alloc<int64_t>(n);
+    g->row_ptr = kc_alloc<int64_t>(n + 1, g->stream);
+    g->col = kc_alloc<int32_t>(2 * m, g->stream);
+    g->coo_src = kc_alloc<int32_t>(2 * m, g->stream);
+    g->orig_ids = kc_alloc<int64_t>(n, g->stream);
     KC_CUDA(cudaMemcpyAsync(g->row_ptr, row_ptr, 8 * (n + 1), cudaMemcpyHostToDevice, g->stream));
     if (m) KC_CUDA(cudaMemcpyAsync(g->col, col, 8 * m, cudaMemcpyHostToDevice, g->stream));
     if (n && orig_ids)
@@ -375,10 +399,10 @@ void kc_build_from_csr(kc_graph *g, int64_t n, int64_t m, const int64_t *row_ptr
 }
 
 void kc_free_dag(kc_graph *g) {
-    if (g->rank) cudaFree(g->rank);
-    if (g->orow_ptr) cudaFree(g->orow_ptr);
-    if (g->ocol) cudaFree(g->ocol);
-    if (g->ocoo) cudaFree(g->ocoo);
+    if (g->rank) kc_free(g->rank, g->stream);
+    if (g->orow_ptr) kc_free(g->orow_ptr, g->stream);
+    if (g->ocol) kc_free(g->ocol, g->stream);
+    if (g->ocoo) kc_free(g->ocoo, g->stream);
     g->rank = nullptr;
     g->orow_ptr = nullptr;
     g->ocol = nullptr;
@@ -390,68 +414,46 @@ void kc_free_dag(kc_graph *g) {
 // highest level at which some vertex was removed.
 static void degeneracy_rank(kc_graph *g, int64_t *degeneracy, int64_t *rounds_out) {
     const int64_t n = g->n;
-    int32_t *deg = kc_alloc<int32_t>(n);
-    int32_t *round_of = kc_alloc<int32_t>(n);
-    int32_t *fa = kc_alloc<int32_t>(n);
-    int32_t *fb = kc_alloc<int32_t>(n);
-    int32_t *cnt = kc_alloc<int32_t>(4);  // [0] frontier size, [1] min deg, [2] next size
-    int32_t *h_cnt = nullptr;
-    KC_CUDA(cudaMallocHost(&h_cnt, 4 * sizeof(int32_t)));
-    const int grid = grid_for(n, g->num_sms);
-    k_peel_init<<<grid, kThreads, 0, g->stream>>>(g->row_ptr, n, deg, round_of);
-    KC_CUDA(cudaGetLastError());
-    int64_t removed = 0;
-    int32_t level = 0, round = 0;
-    int64_t degen = 0;
-    const int32_t big = 0x7fffffff;
-    while (removed < n) {
-        int32_t init[3] = {0, big, 0};
-        KC_CUDA(cudaMemcpyAsync(cnt, init, 12, cudaMemcpyHostToDevice, g->stream));
-        k_peel_scan<<<grid, kThreads, 0, g->stream>>>(deg, round_of, n, level, fa, cnt);
-        KC_CUDA(cudaMemcpyAsync(h_cnt, cnt, 8, cudaMemcpyDeviceToHost, g->stream));
-        KC_CUDA(cudaStreamSynchronize(g->stream));
-        int32_t fsize = h_cnt[0];
-        if (fsize == 0) {
-            KC_REQUIRE(h_cnt[1] != big, KC_ECUDA, "k-core peel stalled");
-            level = h_cnt[1];
-            continue;
-        }
-        if (level > degen) degen = level;
-        while (fsize > 0) {
-            k_peel_mark<<<grid_for(fsize, g->num_sms), kThreads, 0, g->stream>>>(fa, cnt, round,
-                                                                                 round_of);
-            KC_CUDA(cudaMemsetAsync(cnt + 2, 0, 4, g->stream));
-            k_peel_relax<<<grid_for(int64_t(fsize) * 32, g->num_sms), kThreads, 0, g->stream>>>(
-                fa, cnt, g->row_ptr, g->col, level, deg, round_of, fb, cnt + 2);
-            KC_CUDA(cudaMemcpyAsync(cnt, cnt + 2, 4, cudaMemcpyDeviceToDevice, g->stream));
-            KC_CUDA(cudaMemcpyAsync(h_cnt, cnt, 4, cudaMemcpyDeviceToHost, g->stream));
-            KC_CUDA(cudaStreamSynchronize(g->stream));
-            removed += fsize;
-            ++round;
-            fsize = h_cnt[0];
-            std::swap(fa, fb);
-        }
-    }
+    KC_REQUIRE(n < (int64_t(1) << 31), KC_EINVAL, "graph too large for 32-bit vertex ids");
+    int32_t *deg = kc_alloc<int32_t>(n, g->stream);
+    int32_t *round_of = kc_alloc<int32_t>(n, g->stream);
+    int32_t *order = kc_alloc<int32_t>(n, g->stream);
+    int32_t *ctl = kc_alloc<int32_t>(8, g->stream);
+    int per_sm = 0;
+    KC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_peel_coop, kThreads, 0));
+    KC_REQUIRE(per_sm > 0, KC_ECUDA, "peel kernel cannot be resident");
+    int grid = per_sm * g->num_sms;
+    const int64_t want = (n + kThreads - 1) / kThreads;
+    if (want < grid) grid = int(want < 1 ? 1 : want);
+    const int64_t *rp = g->row_ptr;
+    const int32_t *cl = g->col;
+    int64_t nn = n;
+    void *args[] = {(void *)&rp, (void *)&cl, (void *)&nn, (void *)&deg, (void *)&round_of,
+                    (void *)&order, (void *)&ctl};
+    KC_CUDA(cudaLaunchCooperativeKernel((void *)k_peel_coop, dim3(grid), dim3(kThreads), args, 0,
+                                        g->stream));
+    int32_t h[8] = {0};
+    KC_CUDA(cudaMemcpyAsync(h, ctl, sizeof(h), cudaMemcpyDeviceToHost, g->stream));
+    KC_CUDA(cudaStreamSynchronize(g->stream));
+    const int32_t round = h[4];
     // rank = position in (round, id) order
     int bits = kc_bits_for(n - 1 > 0 ? n - 1 : 1);
     int rbits = kc_bits_for(round > 0 ? round : 1);
     KC_REQUIRE(bits + rbits <= 64, KC_EINVAL, "too many peel rounds");
-    uint64_t *keys = kc_alloc<uint64_t>(n);
-    uint64_t *keys2 = kc_alloc<uint64_t>(n);
-    k_peel_keys<<<grid, kThreads, 0, g->stream>>>(round_of, n, bits, keys);
+    uint64_t *keys = kc_alloc<uint64_t>(n, g->stream);
+    uint64_t *keys2 = kc_alloc<uint64_t>(n, g->stream);
+    const int g1 = grid_for(n, g->num_sms);
+    k_peel_keys<<<g1, kThreads, 0, g->stream>>>(round_of, n, bits, keys);
     sort_u64(g, keys, keys2, n, bits + rbits);
-    k_rank_from_sorted<<<grid, kThreads, 0, g->stream>>>(keys2, n, bits, g->rank);
+    k_rank_from_sorted<<<g1, kThreads, 0, g->stream>>>(keys2, n, bits, g->rank);
     KC_CUDA(cudaGetLastError());
-    KC_CUDA(cudaStreamSynchronize(g->stream));
-    cudaFree(keys);
-    cudaFree(keys2);
-    cudaFree(deg);
-    cudaFree(round_of);
-    cudaFree(fa);
-    cudaFree(fb);
-    cudaFree(cnt);
-    cudaFreeHost(h_cnt);
-    *degeneracy = degen;
+    kc_free(keys, g->stream);
+    kc_free(keys2, g->stream);
+    kc_free(deg, g->stream);
+    kc_free(round_of, g->stream);
+    kc_free(order, g->stream);
+    kc_free(ctl, g->stream);
+    *degeneracy = h[3];
     *rounds_out = round;
 }
 
@@ -462,7 +464,7 @@ void kc_do_orient(kc_graph *g, int criterion, const int32_t *rank_in, kc_dag_inf
     KC_REQUIRE(criterion != KC_CRIT_GIVEN || rank_in, KC_EINVAL, "rank_in required");
     kc_free_dag(g);
     const int64_t n = g->n, two_m = 2 * g->m;
-    g->rank = kc_alloc<int32_t>(n);
+    g->rank = kc_alloc<int32_t>(n, g->stream);
     int64_t degen = -1, rounds = 0;
     EventTimer t_rank(g->stream);
     if (n > 0) {
@@ -471,15 +473,15 @@ void kc_do_orient(kc_graph *g, int criterion, const int32_t *rank_in, kc_dag_inf
             // orientation.py:124-128: lexsort((arange(n), degrees))
             int bits = kc_bits_for(n - 1 > 0 ? n - 1 : 1);
             int dbits = kc_bits_for(g->d_max_und > 0 ? g->d_max_und : 1);
-            uint64_t *keys = kc_alloc<uint64_t>(n);
-            uint64_t *keys2 = kc_alloc<uint64_t>(n);
+            uint64_t *keys = kc_alloc<uint64_t>(n, g->stream);
+            uint64_t *keys2 = kc_alloc<uint64_t>(n, g->stream);
             k_degree_keys<<<grid, kThreads, 0, g->stream>>>(g->row_ptr, n, bits, keys);
             sort_u64(g, keys, keys2, n, bits + dbits);
             k_rank_from_sorted<<<grid, kThreads, 0, g->stream>>>(keys2, n, bits, g->rank);
             KC_CUDA(cudaGetLastError());
             KC_CUDA(cudaStreamSynchronize(g->stream));
-            cudaFree(keys);
-            cudaFree(keys2);
+            kc_free(keys, g->stream);
+            kc_free(keys2, g->stream);
         } else if (criterion == KC_CRIT_DEGENERACY) {
             degeneracy_rank(g, &degen, &rounds);
         } else {
@@ -491,9 +493,9 @@ void kc_do_orient(kc_graph *g, int criterion, const int32_t *rank_in, kc_dag_inf
     double rank_ms = t_rank.stop();
 
     EventTimer t_orient(g->stream);
-    g->orow_ptr = kc_alloc<int64_t>(n + 1);
-    g->ocol = kc_alloc<int32_t>(g->m);
-    g->ocoo = kc_alloc<int32_t>(g->m);
+    g->orow_ptr = kc_alloc<int64_t>(n + 1, g->stream);
+    g->ocol = kc_alloc<int32_t>(g->m, g->stream);
+    g->ocoo = kc_alloc<int32_t>(g->m, g->stream);
     int64_t m_dir = 0;
     unsigned long long d_max = 0;
     if (n == 0) {
@@ -501,8 +503,8 @@ void kc_do_orient(kc_graph *g, int criterion, const int32_t *rank_in, kc_dag_inf
     } else if (two_m == 0) {
         KC_CUDA(cudaMemsetAsync(g->orow_ptr, 0, 8 * (n + 1), g->stream));
     } else {
-        uint8_t *flags = kc_alloc<uint8_t>(two_m);
-        int32_t *d_cnt = kc_alloc<int32_t>(1);
+        uint8_t *flags = kc_alloc<uint8_t>(two_m, g->stream);
+        int32_t *d_cnt = kc_alloc<int32_t>(1, g->stream);
         k_orient_flags<<<grid_for(two_m, g->num_sms), kThreads, 0, g->stream>>>(
             g->col, g->coo_src, g->rank, two_m, flags);
         size_t bytes = 0;
@@ -519,16 +521,16 @@ void kc_do_orient(kc_graph *g, int criterion, const int32_t *rank_in, kc_dag_inf
         m_dir = h;
         k_row_ptr<<<grid_for(n + 1, g->num_sms), kThreads, 0, g->stream>>>(g->ocoo, m_dir, n,
                                                                             g->orow_ptr);
-        unsigned long long *d_dmax = kc_alloc<unsigned long long>(1);
+        unsigned long long *d_dmax = kc_alloc<unsigned long long>(1, g->stream);
         KC_CUDA(cudaMemsetAsync(d_dmax, 0, 8, g->stream));
         k_out_degree_max<<<grid_for(n, g->num_sms), kThreads, 0, g->stream>>>(g->orow_ptr, n,
                                                                                d_dmax);
         KC_CUDA(cudaMemcpyAsync(&d_max, d_dmax, 8, cudaMemcpyDeviceToHost, g->stream));
         KC_CUDA(cudaGetLastError());
         KC_CUDA(cudaStreamSynchronize(g->stream));
-        cudaFree(d_dmax);
-        cudaFree(flags);
-        cudaFree(d_cnt);
+        kc_free(d_dmax, g->stream);
+        kc_free(flags, g->stream);
+        kc_free(d_cnt, g->stream);
     }
     double orient_ms = t_orient.stop();
     g->m_dir = m_dir;
@@ -549,8 +551,8 @@ void kc_do_orient(kc_graph *g, int criterion, const int32_t *rank_in, kc_dag_inf
 int64_t kc_task_count(const kc_graph *g, int scheme) {
     if (scheme == KC_SCHEME_EDGE) return g->m_dir;
     if (g->n == 0) return 0;
-    int32_t *flag = kc_alloc<int32_t>(g->n);
-    int32_t *out = kc_alloc<int32_t>(1);
+    int32_t *flag = kc_alloc<int32_t>(g->n, g->stream);
+    int32_t *out = kc_alloc<int32_t>(1, g->stream);
     k_vertex_task_flags<<<grid_for(g->n, g->num_sms), kThreads, 0, g->stream>>>(g->orow_ptr, g->n,
                                                                                  flag);
     size_t bytes = 0;
@@ -560,7 +562,7 @@ int64_t kc_task_count(const kc_graph *g, int scheme) {
     int32_t h = 0;
     KC_CUDA(cudaMemcpyAsync(&h, out, 4, cudaMemcpyDeviceToHost, g->stream));
     KC_CUDA(cudaStreamSynchronize(g->stream));
-    cudaFree(flag);
-    cudaFree(out);
+    kc_free(flag, g->stream);
+    kc_free(out, g->stream);
     return h;
 }

@@ -74,16 +74,26 @@ struct kc_device_guard {
 void *kc_tmp(kc_graph *g, size_t bytes);
 void kc_free_dag(kc_graph *g);
 
+// Device memory comes from the stream-ordered pool (cudaMallocAsync on the
+// graph's stream; the pool keeps freed blocks, so repeated runs do not pay
+// cudaMalloc/cudaFree or their implicit device synchronisation).
 template <typename T>
-static inline T *kc_alloc(size_t count) {
+static inline T *kc_alloc(size_t count, cudaStream_t s) {
     T *p = nullptr;
     if (count == 0) count = 1;
-    cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void **>(&p), count * sizeof(T), s);
     if (e != cudaSuccess)
         throw kc_error(e == cudaErrorMemoryAllocation ? KC_ENOMEM : KC_ECUDA,
-                       std::string("cudaMalloc: ") + cudaGetErrorString(e));
+                       std::string("cudaMallocAsync: ") + cudaGetErrorString(e));
     return p;
 }
+
+static inline void kc_free(void *p, cudaStream_t s) {
+    if (p) cudaFreeAsync(p, s);
+}
+
+// keep freed pool memory for reuse (called once per device)
+void kc_pool_setup(int device);
 
 static inline int kc_bits_for(int64_t x) {  // bits needed to hold 0..x
     int b = 1;

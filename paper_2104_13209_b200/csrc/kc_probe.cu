@@ -62,7 +62,8 @@ void kc_do_probe(int device, double *reg_wps, double *smem_wps, double *sm_mhz) 
     int sms = 0, clk_khz = 0;
     KC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
     KC_CUDA(cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, device));
-    unsigned long long *sink = kc_alloc<unsigned long long>(1);
+    unsigned long long *sink = nullptr;
+    KC_CUDA(cudaMalloc(&sink, sizeof(unsigned long long)));
     cudaEvent_t e0, e1;
     KC_CUDA(cudaEventCreate(&e0));
     KC_CUDA(cudaEventCreate(&e1));

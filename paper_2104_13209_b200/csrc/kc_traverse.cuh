@@ -1,0 +1,384 @@
+// kc_traverse.cuh -- warp-level search-tree traversals (K5 orient, K6/K7 pivot).
+//
+// One warp walks one level-1 subtree of a task's induced sub-graph.  A
+// candidate set over the d locals is a *lane-distributed bitset*: lane l holds
+// words l, l+32, ... (WPL words per lane, W = ceil(d/32) <= 32*WPL), so
+// AND-ing a set with a bitmap row is one coalesced shared-memory load per lane
+// and emptiness / next-vertex selection are __ballot_sync + __ffs + __shfl_sync
+// (PAPER.md:405-418, :461-465).  Local ids ascend with (word, bit), so
+// next_bit() enumerates a set in ascending local id -- the reference's order
+// (engine_orient.py:51-60, engine_pivot.py:140-150).
+//
+// The hot primitive of both engines is "score every v of a set C against C":
+//   orient, last level (engine_orient.py:64-69): sum_v popc(C & row v)
+//   pivot selection  (engine_pivot.py:82-101):   argmax_v popc(C & row v)
+// It runs lane-parallel over v (C compacted into a per-warp list, lane j takes
+// the j-th member) and word-sparse over C: only the nonzero words of C
+// (one ballot) are visited, each broadcast from its owner lane by __shfl_sync.
+//
+// Frames of the explicit DFS stack hold only the candidate set (and, for the
+// pivot engine, the branch set and two scalars); the "remaining" cursor set is
+// recomputed from the last expanded vertex, so a frame is 32*WPL (+32*WPL+4)
+// words.  The first `nsm` frames of a warp live in shared memory, deeper
+// ones in a per-warp global slot (L1-cached).
+#pragma once
+
+#include "kc_internal.cuh"
+
+namespace kct {
+
+typedef unsigned long long ull;
+constexpr unsigned FULL = 0xffffffffu;
+
+template <int WPL>
+struct Set {
+    uint32_t w[WPL];
+};
+
+// bits of a 32-bit word (local ids w*32 .. w*32+31) strictly above local id c
+__device__ __forceinline__ uint32_t above_mask(int word, int c) {
+    const int lo = word << 5;
+    if (c < lo) return FULL;
+    if (c >= lo + 31) return 0u;
+    return ~((2u << (c - lo)) - 1u);
+}
+// bits strictly below local id v
+__device__ __forceinline__ uint32_t below_mask(int word, int v) {
+    const int lo = word << 5;
+    if (v >= lo + 32) return FULL;
+    if (v <= lo) return 0u;
+    return (1u << (v - lo)) - 1u;
+}
+
+template <int WPL>
+__device__ __forceinline__ Set<WPL> load_row(const uint32_t *__restrict__ rows, int RS, int W,
+                                             int v, int lane) {
+    Set<WPL> r;
+    const uint32_t *rv = rows + v * RS;
+#pragma unroll
+    for (int p = 0; p < WPL; ++p) {
+        const int w = p * 32 + lane;
+        r.w[p] = w < W ? rv[w] : 0u;
+    }
+    return r;
+}
+
+template <int WPL>
+__device__ __forceinline__ bool any_set(const Set<WPL> &s) {
+    uint32_t x = 0;
+#pragma unroll
+    for (int p = 0; p < WPL; ++p) x |= s.w[p];
+    return __ballot_sync(FULL, x != 0) != 0;
+}
+
+template <int WPL>
+__device__ __forceinline__ int popc_set(const Set<WPL> &s) {  // per-lane part
+    int c = 0;
+#pragma unroll
+    for (int p = 0; p < WPL; ++p) c += __popc(s.w[p]);
+    return c;
+}
+
+// lowest member of R (ascending local id), removed from R; -1 if empty
+template <int WPL>
+__device__ __forceinline__ int next_bit(Set<WPL> &R, int lane) {
+#pragma unroll
+    for (int p = 0; p < WPL; ++p) {
+        const unsigned b = __ballot_sync(FULL, R.w[p] != 0);
+        if (b) {
+            const int L = __ffs(b) - 1;
+            const uint32_t x = __shfl_sync(FULL, R.w[p], L);
+            if (lane == L) R.w[p] = x & (x - 1u);
+            return ((p * 32 + L) << 5) + __ffs(x) - 1;
+        }
+    }
+    return -1;
+}
+
+// compact the members of C (ascending) into list[0..n); returns n (uniform)
+template <int WPL>
+__device__ __forceinline__ int compact(const Set<WPL> &C, int *list, int lane) {
+    int n = 0;
+#pragma unroll
+    for (int p = 0; p < WPL; ++p) {
+        uint32_t x = C.w[p];
+        const int c = __popc(x);
+        int incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl += y;
+        }
+        int off = n + incl - c;
+        const int base = (p * 32 + lane) << 5;
+        while (x) {
+            list[off++] = base + __ffs(x) - 1;
+            x &= x - 1u;
+        }
+        n += __shfl_sync(FULL, incl, 31);
+    }
+    __syncwarp();
+    return n;
+}
+
+// popc(C & row v) for this lane's v (valid) over the nonzero words of C.
+// All lanes must call it (shuffles); invalid lanes pass v = 0, valid = false.
+template <int WPL>
+__device__ __forceinline__ int cover(const uint32_t *__restrict__ rows, int RS,
+                                     const Set<WPL> &C, int v, bool valid) {
+    int cov = 0;
+    const uint32_t *rv = rows + v * RS;
+#pragma unroll
+    for (int p = 0; p < WPL; ++p) {
+        unsigned nz = __ballot_sync(FULL, C.w[p] != 0);
+        while (nz) {
+            const int L = __ffs(nz) - 1;
+            nz &= nz - 1u;
+            const uint32_t cw = __shfl_sync(FULL, C.w[p], L);
+            if (valid) cov += __popc(cw & rv[p * 32 + L]);
+        }
+    }
+    return cov;
+}
+
+// sum over v in C of popc(C & row v); the sum lands in the calling lanes'
+// accumulators (reduced at kernel end).  Returns |C| (uniform).
+template <int WPL>
+__device__ __forceinline__ int score_sum(const uint32_t *__restrict__ rows, int RS,
+                                         const Set<WPL> &C, int *list, int lane, ull &acc,
+                                         ull &work, int W) {
+    const int n = compact<WPL>(C, list, lane);
+    for (int base = 0; base < n; base += 32) {
+        const int i = base + lane;
+        const bool ok = i < n;
+        const int v = ok ? list[i] : 0;
+        acc += ull(cover<WPL>(rows, RS, C, v, ok));
+    }
+    if (lane == 0) work += ull(n) * W;
+    __syncwarp();
+    return n;
+}
+
+// argmax over v in C of popc(C & row v), lowest v on ties (engine_pivot.py:82-101)
+template <int WPL>
+__device__ __forceinline__ int select_pivot(const uint32_t *__restrict__ rows, int RS,
+                                            const Set<WPL> &C, int *list, int lane, ull &work,
+                                            int W) {
+    const int n = compact<WPL>(C, list, lane);
+    ull best = 0;
+    for (int base = 0; base < n; base += 32) {
+        const int i = base + lane;
+        const bool ok = i < n;
+        const int v = ok ? list[i] : 0;
+        const int cov = cover<WPL>(rows, RS, C, v, ok);
+        const ull key = ok ? ((ull(cov + 1) << 32) | ull(0xffffffffu - uint32_t(v))) : 0ull;
+        best = key > best ? key : best;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        const ull y = __shfl_xor_sync(FULL, best, o);
+        best = y > best ? y : best;
+    }
+    if (lane == 0) work += ull(n) * W;
+    __syncwarp();
+    return int(0xffffffffu - uint32_t(best & 0xffffffffull));
+}
+
+// ---------------------------------------------------------------------------
+// frames
+// ---------------------------------------------------------------------------
+struct Frames {
+    uint32_t *sm;  // frames [0, nsm)
+    uint32_t *gm;  // frames [nsm, ...)
+    int nsm;
+    int fw;  // words per frame
+    __device__ __forceinline__ uint32_t *at(int s) const {
+        return s < nsm ? sm + s * fw : gm + int64_t(s - nsm) * fw;
+    }
+};
+
+template <int WPL>
+__device__ __forceinline__ void store_set(uint32_t *f, const Set<WPL> &S, int lane) {
+#pragma unroll
+    for (int p = 0; p < WPL; ++p) f[p * 32 + lane] = S.w[p];
+}
+template <int WPL>
+__device__ __forceinline__ Set<WPL> load_set(const uint32_t *f, int lane) {
+    Set<WPL> S;
+#pragma unroll
+    for (int p = 0; p < WPL; ++p) S.w[p] = f[p * 32 + lane];
+    return S;
+}
+
+// ---------------------------------------------------------------------------
+// orient: one level-1 subtree (engine_orient.py:32-79).  The caller expanded
+// root-level vertex u (and counted its visit); C = row(u) is frame 1.
+// last = t - 2 >= 1.  Orient frame layout: [C: 32*WPL][cursor].
+// ---------------------------------------------------------------------------
+template <int WPL>
+__device__ void orient_subtree(const uint32_t *__restrict__ rows, int RS, int W, int last, int u,
+                               const Frames &F, int *list, ull &acc, ull &visits, ull &work) {
+    const int lane = threadIdx.x & 31;
+    Set<WPL> C = load_row<WPL>(rows, RS, W, u, lane);
+    if (last == 1) {  // frame 1 is the last level
+        visits += ull(popc_set<WPL>(C));
+        score_sum<WPL>(rows, RS, C, list, lane, acc, work, W);
+        return;
+    }
+    if (!any_set<WPL>(C)) return;
+    int s = 1;
+    Set<WPL> R = C;
+    store_set<WPL>(F.at(1), C, lane);
+    const int cur = 32 * WPL;  // cursor word offset inside a frame
+    for (;;) {
+        const int v = next_bit<WPL>(R, lane);
+        if (v < 0) {
+            if (--s == 0) break;
+            const uint32_t *f = F.at(s);
+            C = load_set<WPL>(f, lane);
+            const int c = int(f[cur]);
+#pragma unroll
+            for (int p = 0; p < WPL; ++p) R.w[p] = C.w[p] & above_mask(p * 32 + lane, c);
+            continue;
+        }
+        if (lane == 0) {
+            ++visits;
+            work += W;
+        }
+        Set<WPL> X;
+        const uint32_t *rv = rows + v * RS;
+#pragma unroll
+        for (int p = 0; p < WPL; ++p) {
+            const int w = p * 32 + lane;
+            X.w[p] = w < W ? (C.w[p] & rv[w]) : 0u;
+        }
+        if (s + 1 == last) {
+            visits += ull(popc_set<WPL>(X));
+            score_sum<WPL>(rows, RS, X, list, lane, acc, work, W);
+            continue;
+        }
+        if (!any_set<WPL>(X)) continue;
+        uint32_t *f = F.at(s);
+        if (lane == 0) f[cur] = uint32_t(v);
+        ++s;
+        C = X;
+        R = X;
+        store_set<WPL>(F.at(s), C, lane);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// pivot: one root-level branch v0 (engine_pivot.py:117-233).  The caller
+// passes the root frame's sets S0 (all locals) and P0 (branch set) via smem
+// pointers.  Pivot frame layout: [C: 32*WPL][P: 32*WPL][piv, npv, cursor, -].
+// Leaves are binned as hist[(path length, pivots)] (expanded exactly on the
+// host).  t: target; allk: no stopping rule.
+// ---------------------------------------------------------------------------
+struct PivotLeafSink {
+    ull *s_hist;   // shared triangular histogram for len < sh_hl
+    int sh_hl;
+    ull *g_hist;   // global L x L histogram
+    int L;
+    __device__ __forceinline__ void add(int len, int np) const {
+        if (len < sh_hl) atomicAdd(&s_hist[len * (len + 1) / 2 + np], 1ull);
+        else atomicAdd(&g_hist[int64_t(len) * L + np], 1ull);
+    }
+};
+
+template <int WPL>
+__device__ void pivot_subtree(const uint32_t *__restrict__ rows, int RS, int W, int t, bool allk,
+                              int v0, int piv0, const uint32_t *S0, const uint32_t *P0,
+                              const Frames &F, int *list, const PivotLeafSink &sink, ull &visits,
+                              ull &work) {
+    const int lane = threadIdx.x & 31;
+    const int np0 = v0 == piv0 ? 1 : 0;
+    if (!allk && 1 - t > np0) return;  // engine_pivot.py:152-153
+    if (lane == 0) {
+        ++visits;
+        work += W;
+    }
+    Set<WPL> C;
+    {
+        const uint32_t *rv = rows + v0 * RS;
+#pragma unroll
+        for (int p = 0; p < WPL; ++p) {
+            const int w = p * 32 + lane;
+            C.w[p] = w < W ? (S0[w] & rv[w] & ~(P0[w] & below_mask(w, v0))) : 0u;
+        }
+    }
+    if (!any_set<WPL>(C)) {
+        if ((allk || 1 >= t) && lane == 0) sink.add(1, np0);
+        return;
+    }
+    const int PO = 32 * WPL, SC = 64 * WPL;  // P offset, scalars offset
+    int s = 1;
+    int npv = np0;
+    int piv = select_pivot<WPL>(rows, RS, C, list, lane, work, W);
+    Set<WPL> P;
+    {
+        const Set<WPL> rp = load_row<WPL>(rows, RS, W, piv, lane);
+#pragma unroll
+        for (int p = 0; p < WPL; ++p) P.w[p] = C.w[p] & ~rp.w[p];
+    }
+    Set<WPL> R = P;
+    {
+        uint32_t *f = F.at(1);
+        store_set<WPL>(f, C, lane);
+        store_set<WPL>(f + PO, P, lane);
+        if (lane == 0) {
+            f[SC] = uint32_t(piv);
+            f[SC + 1] = uint32_t(npv);
+        }
+    }
+    for (;;) {
+        const int v = next_bit<WPL>(R, lane);
+        if (v < 0) {
+            if (--s == 0) break;
+            const uint32_t *f = F.at(s);
+            C = load_set<WPL>(f, lane);
+            P = load_set<WPL>(f + PO, lane);
+            piv = int(f[SC]);
+            npv = int(f[SC + 1]);
+            const int c = int(f[SC + 2]);
+#pragma unroll
+            for (int p = 0; p < WPL; ++p) R.w[p] = P.w[p] & above_mask(p * 32 + lane, c);
+            continue;
+        }
+        const int np2 = npv + (v == piv ? 1 : 0);
+        if (!allk && s + 1 - t > np2) continue;
+        if (lane == 0) {
+            ++visits;
+            work += W;
+        }
+        Set<WPL> X;
+        const uint32_t *rv = rows + v * RS;
+#pragma unroll
+        for (int p = 0; p < WPL; ++p) {
+            const int w = p * 32 + lane;
+            // engine_pivot.py:158-166: drop already-branched pivot-set bits below v
+            X.w[p] = w < W ? (C.w[p] & rv[w] & ~(P.w[p] & below_mask(w, v))) : 0u;
+        }
+        if (any_set<WPL>(X)) {
+            if (lane == 0) F.at(s)[SC + 2] = uint32_t(v);
+            ++s;
+            npv = np2;
+            C = X;
+            piv = select_pivot<WPL>(rows, RS, C, list, lane, work, W);
+            const Set<WPL> rp = load_row<WPL>(rows, RS, W, piv, lane);
+#pragma unroll
+            for (int p = 0; p < WPL; ++p) P.w[p] = C.w[p] & ~rp.w[p];
+            R = P;
+            uint32_t *f = F.at(s);
+            store_set<WPL>(f, C, lane);
+            store_set<WPL>(f + PO, P, lane);
+            if (lane == 0) {
+                f[SC] = uint32_t(piv);
+                f[SC + 1] = uint32_t(npv);
+            }
+        } else if (allk || s + 1 >= t) {
+            if (lane == 0) sink.add(s + 1, np2);
+        }
+    }
+}
+
+}  // namespace kct

@@ -76,7 +76,8 @@ def main():
                                "cliques_per_s": rep.count / (tot / 1e3) if tot else None,
                                "d_max": rep.d_max, "degeneracy": rep.degeneracy,
                                "visits": rep.load.total,
-                               "normalized_max": round(rep.load.normalized_max, 3)}
+                               "normalized_max": round(rep.load.normalized_max, 3),
+                               "counters": rep.counters}
                         if a.all_k and rep.counts:
                             out["counts"] = {str(kk): str(v) for kk, v in rep.counts.items()}
                         if a.oracle_workers:
