@@ -82,6 +82,7 @@ void destroy(kc_graph *g) {
         cudaStreamSynchronize(g->stream);
         cudaStreamDestroy(g->stream);
     }
+    if (g->aux) cudaStreamDestroy(g->aux);
     if (prev >= 0) cudaSetDevice(prev);
     delete g;
 }

@@ -25,6 +25,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <memory>
 #include <vector>
 
 #include "kc_internal.cuh"
@@ -235,7 +236,8 @@ __device__ void flush_block(const CountParams &p, ull acc, ull visits, ull tasks
 // ---------------------------------------------------------------------------
 template <int BLOCK, int WPL>
 __device__ void orient_task(const CountParams &p, const uint32_t *rows, int d,
-                            const kct::Frames &F, int *list, int *s_next, ull &acc, ull &visits,
+                            const kct::Frames &F, int *list, uint32_t *cbuf,
+                            const kct::SmallScratch &SS, int *s_next, ull &acc, ull &visits,
                             ull &work) {
     const int W = (d + 31) >> 5, RS = row_stride(W);
     const int last = p.t - 2;
@@ -261,7 +263,7 @@ __device__ void orient_task(const CountParams &p, const uint32_t *rows, int d,
             ++visits;
             work += ull(W);
         }
-        kct::orient_subtree<WPL>(rows, RS, W, last, u, F, list, acc, visits, work);
+        kct::orient_subtree<WPL>(rows, RS, W, last, u, F, list, cbuf, SS, acc, visits, work);
     }
 }
 
@@ -271,7 +273,7 @@ __device__ void orient_task(const CountParams &p, const uint32_t *rows, int d,
 template <int BLOCK, int WPL>
 __device__ void pivot_task(const CountParams &p, const uint32_t *rows, int d, uint32_t *S0,
                            uint32_t *P0, const kct::Frames &F, int *list,
-                           const kct::PivotLeafSink &sink, int *s_next, int *s_piv0, ull *s_key,
+                           const kct::SmallScratch &SS, const kct::PivotLeafSink &sink, int *s_next, int *s_piv0, ull *s_key,
                            ull &visits, ull &work) {
     constexpr int NW = BLOCK / 32;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -313,8 +315,8 @@ __device__ void pivot_task(const CountParams &p, const uint32_t *rows, int d, ui
         v = __shfl_sync(kct::FULL, v, 0);
         if (v >= d) break;
         if (!((P0[v >> 5] >> (v & 31)) & 1u)) continue;
-        kct::pivot_subtree<WPL>(rows, RS, W, p.t, p.all_k != 0, v, piv0, S0, P0, F, list, sink,
-                                visits, work);
+        kct::pivot_subtree<WPL>(rows, RS, W, p.t, p.all_k != 0, v, piv0, S0, P0, F, list, SS,
+                                sink, visits, work);
     }
 }
 
@@ -347,10 +349,15 @@ __global__ void __launch_bounds__(BLOCK) k_count(CountParams p) {
     int32_t *scratch = reinterpret_cast<int32_t *>(area);  // edge-scheme staging (pre-traversal)
     uint32_t *S0 = area, *P0 = area + 32 * WPL;
     if (MODE == MODE_PIVOT) area += 64 * WPL;
-    const int per_warp = ((p.dcap + 3) & ~3) + p.nsm_frames * p.fw;
+    const int per_warp =
+        ((p.dcap + 3) & ~3) + 32 * WPL + kct::kSmallWords + p.nsm_frames * p.fw;
     int *list = reinterpret_cast<int *>(area + warp * per_warp);
+    uint32_t *cbuf = area + warp * per_warp + ((p.dcap + 3) & ~3);
+    kct::SmallScratch SS;
+    SS.srow = cbuf + 32 * WPL;
+    SS.sstk = SS.srow + 32;
     kct::Frames F;
-    F.sm = area + warp * per_warp + ((p.dcap + 3) & ~3);
+    F.sm = SS.srow + kct::kSmallWords;
     F.nsm = p.nsm_frames;
     F.fw = p.fw;
     F.gm = p.frames_global ? p.frames_global + (int64_t(blockIdx.x) * NW + warp) * p.frames_slot
@@ -406,9 +413,9 @@ __global__ void __launch_bounds__(BLOCK) k_count(CountParams p) {
             continue;
         }
         if (MODE == MODE_ORIENT) {
-            orient_task<BLOCK, WPL>(p, rows, d, F, list, &s_next, acc, visits, work);
+            orient_task<BLOCK, WPL>(p, rows, d, F, list, cbuf, SS, &s_next, acc, visits, work);
         } else {
-            pivot_task<BLOCK, WPL>(p, rows, d, S0, P0, F, list, sink, &s_next, &s_piv0, s_key,
+            pivot_task<BLOCK, WPL>(p, rows, d, S0, P0, F, list, SS, sink, &s_next, &s_piv0, s_key,
                                    visits, work);
         }
     }
@@ -427,6 +434,201 @@ __global__ void __launch_bounds__(BLOCK) k_count(CountParams p) {
         }
     }
     if (MODE != MODE_EXTRACT) flush_block<BLOCK>(p, acc, visits, tasks, work, bytes, s_red);
+}
+
+// ---------------------------------------------------------------------------
+// warp-per-task kernel for small tasks (d <= kWarpD): no CTA barriers, every
+// warp fetches, extracts and walks its own tasks (PAPER.md:461-465 sub-block
+// partitioning taken to one task per warp).  Tasks with d <= 32 run entirely
+// in the S-tier (their rows already are one word).
+// ---------------------------------------------------------------------------
+constexpr int kWarpD = 128;
+
+__device__ __forceinline__ bool gl_contains(const int32_t *__restrict__ a, int n, int32_t x) {
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (__ldg(a + mid) < x) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo < n && __ldg(a + lo) == x;
+}
+
+// warp-level K4: locals + bit matrix of one task (d <= kWarpD)
+__device__ int warp_build(const CountParams &p, int32_t task, int32_t *l2g, uint32_t *rows,
+                          bool need_rows, bool directed, ull &bytes) {
+    const int lane = threadIdx.x & 31;
+    int d;
+    if (p.scheme == KC_SCHEME_VERTEX) {
+        const int64_t beg = p.orow[task];
+        d = int(p.orow[task + 1] - beg);
+        for (int i = lane; i < d; i += 32) l2g[i] = p.ocol[beg + i];
+        if (lane == 0) bytes += 4 + 16 + 4ull * d;
+    } else {
+        const int32_t u = p.ocoo[task], v = p.ocol[task];
+        int64_t ab = p.orow[u], ae = p.orow[u + 1], bb = p.orow[v], be = p.orow[v + 1];
+        if (ae - ab > be - bb) {
+            int64_t t0 = ab, t1 = ae;
+            ab = bb; ae = be; bb = t0; be = t1;
+        }
+        const int la = int(ae - ab), lb = int(be - bb);
+        if (lane == 0) bytes += 4 + 8 + 32 + 4ull * la + 4ull * (lb < la ? lb : la) * 4;
+        d = 0;
+        for (int c = 0; c < la; c += 32) {
+            const int i = c + lane;
+            const int32_t x = i < la ? p.ocol[ab + i] : 0;
+            const bool f = i < la && gl_contains(p.ocol + bb, lb, x);
+            const unsigned m = __ballot_sync(kct::FULL, f);
+            if (f) l2g[d + __popc(m & ((1u << lane) - 1u))] = x;
+            d += __popc(m);
+        }
+    }
+    __syncwarp();
+    if (!need_rows || d == 0) return d;
+    const int W = (d + 31) >> 5, RS = row_stride(W);
+    for (int i = lane; i < d * RS; i += 32) rows[i] = 0u;
+    __syncwarp();
+    const int32_t lo_id = l2g[0], hi_id = l2g[d - 1];
+    for (int i = 0; i < d; ++i) {
+        const int32_t gi = l2g[i];
+        const int64_t beg = p.orow[gi], end = p.orow[gi + 1];
+        if (lane == 0) bytes += 16 + 4ull * (end - beg);
+        for (int64_t e = beg + lane; e < end; e += 32) {
+            const int32_t x = p.ocol[e];
+            if (x < lo_id || x > hi_id) continue;
+            const int j = smem_find(l2g, d, x);
+            if (j >= 0) {
+                atomicOr(&rows[i * RS + (j >> 5)], 1u << (j & 31));
+                if (!directed) atomicOr(&rows[j * RS + (i >> 5)], 1u << (i & 31));
+            }
+        }
+    }
+    __syncwarp();
+    return d;
+}
+
+template <int BLOCK, int MODE>
+__global__ void __launch_bounds__(BLOCK) k_count_warp(CountParams p) {
+    constexpr int NW = BLOCK / 32;
+    constexpr int D = kWarpD, WPL = 1;
+    constexpr int RSD = (D / 32) | 1;
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ ull s_red[4 * NW];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int hist_cells = MODE == MODE_PIVOT ? p.sh_hl * (p.sh_hl + 1) / 2 : 0;
+    ull *s_hist = reinterpret_cast<ull *>(smem);
+    // per warp: l2g[D] rows[D*RSD] list[D] S0[32] P0[32] cbuf[32] small frames
+    const int per_warp = D + D * RSD + D + 32 * 3 + kct::kSmallWords + p.nsm_frames * p.fw;
+    uint32_t *base = reinterpret_cast<uint32_t *>(smem + 8 * hist_cells) + warp * per_warp;
+    int32_t *l2g = reinterpret_cast<int32_t *>(base);
+    uint32_t *rows = base + D;
+    int *list = reinterpret_cast<int *>(rows + D * RSD);
+    uint32_t *S0 = reinterpret_cast<uint32_t *>(list + D);
+    uint32_t *P0 = S0 + 32;
+    uint32_t *cbuf = P0 + 32;
+    kct::SmallScratch SS;
+    SS.srow = cbuf + 32;
+    SS.sstk = SS.srow + 32;
+    kct::Frames F;
+    F.sm = SS.srow + kct::kSmallWords;
+    F.nsm = p.nsm_frames;
+    F.fw = p.fw;
+    F.gm = p.frames_global ? p.frames_global + (int64_t(blockIdx.x) * NW + warp) * p.frames_slot
+                           : nullptr;
+    kct::PivotLeafSink sink;
+    sink.s_hist = s_hist;
+    sink.sh_hl = p.sh_hl;
+    sink.g_hist = p.hist;
+    sink.L = p.hist_dim;
+    for (int i = tid; i < hist_cells; i += BLOCK) s_hist[i] = 0;
+    __syncthreads();
+
+    ull acc = 0, visits = 0, tasks = 0, work = 0, bytes = 0;
+    const int t = p.t;
+    const bool allk = MODE == MODE_PIVOT && p.all_k;
+    for (;;) {
+        ull i = 0;
+        if (lane == 0) i = atomicAdd(p.task_counter, 1ull);
+        i = __shfl_sync(kct::FULL, i, 0);
+        if (i >= ull(p.n_tasks)) break;
+        const int32_t task = p.tasks[i];
+        const bool need_rows = MODE == MODE_PIVOT || t >= 2;
+        const int d = warp_build(p, task, l2g, rows, need_rows, MODE == MODE_ORIENT, bytes);
+        if (allk) {
+            if (d == 0) continue;
+        } else if (d < t) {
+            continue;
+        }
+        if (lane == 0) ++tasks;
+        if (t <= 1 && !allk) {
+            if (lane == 0) acc += t == 0 ? 1ull : ull(d);
+            continue;
+        }
+        const int W = (d + 31) >> 5, RS = row_stride(W);
+        const uint32_t all = d >= 32 ? kct::FULL : ((1u << d) - 1u);
+        if (MODE == MODE_ORIENT) {
+            const int last = t - 2;
+            if (last == 0) {
+                for (int u = lane; u < d; u += 32) {
+                    const uint32_t *ru = rows + u * RS;
+                    int c = 0;
+                    for (int w = 0; w < W; ++w) c += __popc(ru[w]);
+                    acc += ull(c);
+                    ++visits;
+                    work += ull(W);
+                }
+            } else if (W == 1) {
+                kct::orient_small(rows, all, 0, last, SS.sstk, lane, acc, visits, work);
+            } else {
+                for (int u = 0; u < d; ++u) {
+                    if (lane == 0) {
+                        ++visits;
+                        work += ull(W);
+                    }
+                    kct::orient_subtree<WPL>(rows, RS, W, last, u, F, list, cbuf, SS, acc, visits,
+                                             work);
+                }
+            }
+        } else {
+            if (W == 1) {
+                const uint32_t myrow = lane < d ? rows[lane] : 0u;
+                kct::pivot_small(rows, myrow, all, 0, 0, t, allk, SS.sstk, sink, lane, visits,
+                                 work);
+            } else {
+                // root frame: S0 = all locals, pivot = argmax |row c| (lowest id on ties)
+                kct::Set<WPL> A;
+                {
+                    const int lo = lane << 5;
+                    A.w[0] = lo >= d ? 0u : (lo + 32 <= d ? kct::FULL : ((1u << (d - lo)) - 1u));
+                }
+                const int piv0 = kct::select_pivot<WPL>(rows, RS, A, list, lane, work, W);
+                const uint32_t rp = lane < W ? rows[piv0 * RS + lane] : 0u;
+                S0[lane] = A.w[0];
+                P0[lane] = A.w[0] & ~rp;
+                __syncwarp();
+                for (int v = 0; v < d; ++v) {
+                    if (!((P0[v >> 5] >> (v & 31)) & 1u)) continue;
+                    kct::pivot_subtree<WPL>(rows, RS, W, t, allk, v, piv0, S0, P0, F, list, SS,
+                                            sink, visits, work);
+                }
+            }
+        }
+        __syncwarp();
+    }
+    __syncthreads();
+    if (MODE == MODE_PIVOT) {
+        for (int i = tid; i < hist_cells; i += BLOCK) {
+            ull x = s_hist[i];
+            if (x) {
+                int len = int((sqrtf(8.0f * i + 1.0f) - 1.0f) * 0.5f);
+                while (len * (len + 1) / 2 > i) --len;
+                while ((len + 1) * (len + 2) / 2 <= i) ++len;
+                int np = i - len * (len + 1) / 2;
+                atomicAdd(&p.hist[int64_t(len) * p.hist_dim + np], x);
+            }
+        }
+    }
+    flush_block<BLOCK>(p, acc, visits, tasks, work, bytes, s_red);
 }
 
 // ---------------------------------------------------------------------------
@@ -460,8 +662,20 @@ __global__ void k_edge_select(const int64_t *__restrict__ orow, const int32_t *_
         int64_t du = orow[u + 1] - orow[u], dv = orow[v + 1] - orow[v];
         int64_t b = du < dv ? du : dv;  // |N+(u) ∩ N+(v)| <= min
         keep[e] = e >= lo && e < hi && b >= min_d;
-        key[e] = uint32_t(du * dv > 0xffffffffll ? 0xffffffffll : du * dv);
+        key[e] = uint32_t(b);  // bound on the task's locals: routes it to the warp/CTA kernel
     }
+}
+
+// sorted-descending keys: number of keys > thr (first index with key <= thr)
+__global__ void k_split_point(const uint32_t *__restrict__ keys, int64_t n, uint32_t thr,
+                              int32_t *__restrict__ out) {
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (keys[mid] > thr) lo = mid + 1;
+        else hi = mid;
+    }
+    *out = int32_t(lo);
 }
 
 __global__ void k_iota(int32_t *__restrict__ a, int64_t n) {
@@ -501,8 +715,10 @@ struct DevBuf {
 // Builds the device task list: ids of the tasks in [lo, hi) of make_tasks
 // order with enough locals, sorted by descending cost (largest first keeps the
 // persistent queue balanced).  Returns the count.
-int64_t build_tasks(kc_graph *g, int scheme, int64_t lo, int64_t hi, int min_d, DevBuf &out) {
+int64_t build_tasks(kc_graph *g, int scheme, int64_t lo, int64_t hi, int min_d, DevBuf &out,
+                    uint32_t big_thr, int64_t *n_big) {
     const int64_t N = scheme == KC_SCHEME_EDGE ? g->m_dir : g->n;
+    *n_big = 0;
     if (N == 0) return 0;
     DevBuf keep(N), key(4 * N), key2(4 * N), ids(4 * N), ids2(4 * N), cnt(8);
     if (scheme == KC_SCHEME_VERTEX) {
@@ -549,8 +765,14 @@ int64_t build_tasks(kc_graph *g, int scheme, int64_t lo, int64_t hi, int min_d, 
         KC_CUDA(cub::DeviceRadixSort::SortPairsDescending(
             tmp, bytes, key2.as<uint32_t>(), key.as<uint32_t>(), ids2.as<int32_t>(),
             out.as<int32_t>(), int(n_sel), 0, 32, g->stream));
+        k_split_point<<<1, 1, 0, g->stream>>>(key.as<uint32_t>(), n_sel, big_thr,
+                                              cnt.as<int32_t>() + 1);
+        int32_t nb = 0;
+        KC_CUDA(cudaMemcpyAsync(&nb, cnt.as<int32_t>() + 1, 4, cudaMemcpyDeviceToHost,
+                                g->stream));
+        KC_CUDA(cudaStreamSynchronize(g->stream));
+        *n_big = nb;
     }
-    KC_CUDA(cudaStreamSynchronize(g->stream));
     return n_sel;
 }
 
@@ -566,8 +788,11 @@ int frames_needed(int mode, int t, int dcap) {
     return dcap + 2;
 }
 
+typedef std::vector<std::unique_ptr<DevBuf>> Keep;
+
 template <int MODE, int WPL>
-void launch_wpl(kc_graph *g, CountParams &p, int grid_override) {
+void launch_wpl(kc_graph *g, CountParams &p, int grid_override, Keep &keep,
+                cudaStream_t stream) {
     constexpr int NW = kBlock / 32;
     const size_t hist_bytes = MODE == MODE_PIVOT ? 8 * size_t(p.sh_hl) * (p.sh_hl + 1) / 2 : 0;
     const size_t dpad = size_t((p.dcap + 3) & ~3);
@@ -576,7 +801,8 @@ void launch_wpl(kc_graph *g, CountParams &p, int grid_override) {
     p.fw = MODE == MODE_PIVOT ? 64 * WPL + 4 : 32 * WPL + 4;
     const int need = frames_needed(MODE, p.t, p.dcap);
     auto area_words = [&](int nsm) {
-        size_t w = (MODE == MODE_PIVOT ? 64 * WPL : 0) + size_t(NW) * (dpad + size_t(nsm) * p.fw);
+        size_t w = (MODE == MODE_PIVOT ? 64 * WPL : 0) +
+                   size_t(NW) * (dpad + 32 * WPL + kct::kSmallWords + size_t(nsm) * p.fw);
         if (p.scheme == KC_SCHEME_EDGE) w = std::max(w, dpad);
         return w;
     };
@@ -599,32 +825,69 @@ void launch_wpl(kc_graph *g, CountParams &p, int grid_override) {
     int grid = grid_override > 0 ? grid_override : per_sm * g->num_sms;
     if (p.n_tasks > 0 && int64_t(grid) > p.n_tasks && !grid_override) grid = int(p.n_tasks);
     if (grid < 1) grid = 1;
-    DevBuf rows_g, fr_g;
     if (!p.rows_in_smem) {
         p.rows_slot = int64_t(rows_words);
-        new (&rows_g) DevBuf(4 * rows_words * size_t(grid));
-        p.rows_global = rows_g.as<uint32_t>();
+        keep.emplace_back(new DevBuf(4 * rows_words * size_t(grid)));
+        p.rows_global = keep.back()->as<uint32_t>();
     }
     p.frames_global = nullptr;
     p.frames_slot = 0;
     if (MODE != MODE_EXTRACT && need > nsm) {
         p.frames_slot = int64_t(need - nsm) * p.fw;
-        new (&fr_g) DevBuf(4 * size_t(p.frames_slot) * size_t(grid) * NW);
-        p.frames_global = fr_g.as<uint32_t>();
+        keep.emplace_back(new DevBuf(4 * size_t(p.frames_slot) * size_t(grid) * NW));
+        p.frames_global = keep.back()->as<uint32_t>();
     }
-    kern<<<grid, kBlock, smem, g->stream>>>(p);
+    kern<<<grid, kBlock, smem, stream>>>(p);
     KC_CUDA(cudaGetLastError());
-    KC_CUDA(cudaStreamSynchronize(g->stream));
+}
+
+// warp-per-task kernel for tasks with at most kWarpD locals
+template <int MODE>
+void launch_warp(kc_graph *g, CountParams &p, Keep &keep, cudaStream_t stream) {
+    constexpr int NW = kBlock / 32;
+    constexpr int D = kWarpD, RSD = (kWarpD / 32) | 1;
+    const size_t hist_bytes = MODE == MODE_PIVOT ? 8 * size_t(p.sh_hl) * (p.sh_hl + 1) / 2 : 0;
+    p.fw = MODE == MODE_PIVOT ? 64 + 4 : 32 + 4;
+    const int need = std::max(1, std::min(frames_needed(MODE, p.t, D), D + 2));
+    const size_t fixed = size_t(D) + D * RSD + D + 96 + kct::kSmallWords;
+    int nsm = std::min(need, 8);
+    p.nsm_frames = nsm;
+    const size_t smem = hist_bytes + 4 * size_t(NW) * (fixed + size_t(nsm) * p.fw) + 64;
+    auto kern = k_count_warp<kBlock, MODE>;
+    KC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    int per_sm = 0;
+    KC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBlock, smem));
+    KC_REQUIRE(per_sm > 0, KC_ECUDA, "warp count kernel cannot be resident");
+    int grid = per_sm * g->num_sms;
+    const int64_t want = (p.n_tasks + NW - 1) / NW;
+    if (want < grid) grid = int(want < 1 ? 1 : want);
+    p.frames_global = nullptr;
+    p.frames_slot = 0;
+    if (need > nsm) {
+        p.frames_slot = int64_t(need - nsm) * p.fw;
+        keep.emplace_back(new DevBuf(4 * size_t(p.frames_slot) * size_t(grid) * NW));
+        p.frames_global = keep.back()->as<uint32_t>();
+    }
+    kern<<<grid, kBlock, smem, stream>>>(p);
+    KC_CUDA(cudaGetLastError());
 }
 
 template <int MODE>
-void launch(kc_graph *g, CountParams &p, int grid_override = 0) {
+void launch(kc_graph *g, CountParams &p, int grid_override, Keep &keep, cudaStream_t stream) {
     const int wpl = (p.wcap + 31) / 32;
     KC_REQUIRE(wpl <= 4, KC_EINVAL,
                "oriented max out-degree above 4096 locals is not supported by the bitmap engine");
-    if (MODE == MODE_EXTRACT || wpl <= 1) launch_wpl<MODE, 1>(g, p, grid_override);
-    else if (wpl == 2) launch_wpl<MODE, 2>(g, p, grid_override);
-    else launch_wpl<MODE, 4>(g, p, grid_override);
+    if (MODE == MODE_EXTRACT || wpl <= 1) launch_wpl<MODE, 1>(g, p, grid_override, keep, stream);
+    else if (wpl == 2) launch_wpl<MODE, 2>(g, p, grid_override, keep, stream);
+    else launch_wpl<MODE, 4>(g, p, grid_override, keep, stream);
+}
+
+// launch + wait (single-shot debug entry points)
+template <int MODE>
+void launch_sync(kc_graph *g, CountParams &p, int grid_override) {
+    Keep keep;
+    launch<MODE>(g, p, grid_override, keep, g->stream);
+    KC_CUDA(cudaStreamSynchronize(g->stream));
 }
 
 }  // namespace
@@ -662,7 +925,8 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
     if (lo > hi) lo = hi;
     const int min_d = a->all_k ? 1 : (t > 1 ? t : 1);
     DevBuf tasks;
-    const int64_t n_tasks = build_tasks(g, a->scheme, lo, hi, min_d, tasks);
+    int64_t n_big = 0;
+    const int64_t n_tasks = build_tasks(g, a->scheme, lo, hi, min_d, tasks, kWarpD, &n_big);
 
     DevBuf outs(8 * (10 + size_t(kSmidSlots)));
     KC_CUDA(cudaMemsetAsync(outs.p, 0, 8 * (10 + size_t(kSmidSlots)), g->stream));
@@ -694,15 +958,40 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
     p.word_ops = o + 8 + kSmidSlots;
     p.ext_bytes = o + 9 + kSmidSlots;
 
-    cudaEvent_t e0, e1;
+    cudaEvent_t e0, e1, e_fork, e_join;
     KC_CUDA(cudaEventCreate(&e0));
     KC_CUDA(cudaEventCreate(&e1));
+    KC_CUDA(cudaEventCreateWithFlags(&e_fork, cudaEventDisableTiming));
+    KC_CUDA(cudaEventCreateWithFlags(&e_join, cudaEventDisableTiming));
     KC_CUDA(cudaEventRecord(e0, g->stream));
+    Keep keep;
     if (n_tasks > 0) {
-        if (pivot) {
-            launch<MODE_PIVOT>(g, p);
-        } else {
-            launch<MODE_ORIENT>(g, p);
+        // big tasks (more than kWarpD locals): CTA-cooperative kernel on the
+        // graph stream; small tasks: warp-per-task kernel on the aux stream,
+        // concurrently (it fills SMs as the big-task CTAs retire)
+        const int64_t n_small = n_tasks - n_big;
+        CountParams q = p;
+        if (n_big > 0) {
+            p.n_tasks = n_big;
+            if (pivot) launch<MODE_PIVOT>(g, p, 0, keep, g->stream);
+            else launch<MODE_ORIENT>(g, p, 0, keep, g->stream);
+        }
+        if (n_small > 0) {
+            if (!g->aux) KC_CUDA(cudaStreamCreateWithFlags(&g->aux, cudaStreamNonBlocking));
+            q.tasks = tasks.as<int32_t>() + n_big;
+            q.n_tasks = n_small;
+            q.task_counter = o + 7;
+            cudaStream_t st = n_big > 0 ? g->aux : g->stream;
+            if (n_big > 0) {
+                KC_CUDA(cudaEventRecord(e_fork, g->stream));
+                KC_CUDA(cudaStreamWaitEvent(g->aux, e_fork, 0));
+            }
+            if (pivot) launch_warp<MODE_PIVOT>(g, q, keep, st);
+            else launch_warp<MODE_ORIENT>(g, q, keep, st);
+            if (n_big > 0) {
+                KC_CUDA(cudaEventRecord(e_join, g->aux));
+                KC_CUDA(cudaStreamWaitEvent(g->stream, e_join, 0));
+            }
         }
     }
     KC_CUDA(cudaEventRecord(e1, g->stream));
@@ -711,6 +1000,8 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
     KC_CUDA(cudaEventElapsedTime(&ms, e0, e1));
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
+    cudaEventDestroy(e_fork);
+    cudaEventDestroy(e_join);
 
     std::vector<ull> h(10 + size_t(kSmidSlots));
     KC_CUDA(cudaMemcpyAsync(h.data(), outs.p, 8 * h.size(), cudaMemcpyDeviceToHost, g->stream));
@@ -757,7 +1048,7 @@ void kc_do_extract(kc_graph *g, int scheme, int64_t task, int directed, int64_t 
     p.extract_l2g = l.as<int32_t>();
     p.extract_d = dd.as<int>();
     p.task_counter = outs.as<ull>();
-    launch<MODE_EXTRACT>(g, p, 1);
+    launch_sync<MODE_EXTRACT>(g, p, 1);
     int d = 0;
     KC_CUDA(cudaMemcpyAsync(&d, dd.p, 4, cudaMemcpyDeviceToHost, g->stream));
     KC_CUDA(cudaStreamSynchronize(g->stream));
@@ -843,9 +1134,9 @@ void kc_do_count_bitgraph(int device, const uint64_t *rows64, int64_t d64, int t
     p.visits_per_sm = o + 8;
     try {
         if (pivot) {
-            launch<MODE_PIVOT>(&tmpg, p, 1);
+            launch_sync<MODE_PIVOT>(&tmpg, p, 1);
         } else {
-            launch<MODE_ORIENT>(&tmpg, p, 1);
+            launch_sync<MODE_ORIENT>(&tmpg, p, 1);
         }
     } catch (...) {
         throw;

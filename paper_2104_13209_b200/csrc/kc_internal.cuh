@@ -38,6 +38,7 @@ struct kc_error : std::runtime_error {
 struct kc_graph {
     int device = 0;
     cudaStream_t stream = nullptr;
+    cudaStream_t aux = nullptr;  // second stream for concurrent count kernels
     int num_sms = 0;
     int64_t n = 0, m = 0;
     int64_t d_max_und = 0;

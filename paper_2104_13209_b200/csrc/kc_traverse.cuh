@@ -79,6 +79,19 @@ __device__ __forceinline__ int popc_set(const Set<WPL> &s) {  // per-lane part
     return c;
 }
 
+template <int WPL>
+__device__ __forceinline__ void store_set(uint32_t *f, const Set<WPL> &S, int lane) {
+#pragma unroll
+    for (int p = 0; p < WPL; ++p) f[p * 32 + lane] = S.w[p];
+}
+template <int WPL>
+__device__ __forceinline__ Set<WPL> load_set(const uint32_t *f, int lane) {
+    Set<WPL> S;
+#pragma unroll
+    for (int p = 0; p < WPL; ++p) S.w[p] = f[p * 32 + lane];
+    return S;
+}
+
 // lowest member of R (ascending local id), removed from R; -1 if empty
 template <int WPL>
 __device__ __forceinline__ int next_bit(Set<WPL> &R, int lane) {
@@ -159,6 +172,80 @@ __device__ __forceinline__ int score_sum(const uint32_t *__restrict__ rows, int 
     return n;
 }
 
+// The last TWO orientation levels at once, lane-parallel over v in C
+// (frame last-1 = C): every v in C is a visit, each x in X_v = C & row v is a
+// visit of the last frame contributing popc(X_v & row x).  Lane j owns the
+// j-th member v of C and walks X_v itself (3-way AND + POPC per word), so the
+// per-visit ballot/shuffle work of the sequential walk disappears for the two
+// levels that hold almost all visits.  cbuf: per-warp copy of C (32*WPL words).
+template <int WPL>
+__device__ __forceinline__ void score_pairs(const uint32_t *__restrict__ rows, int RS, int W,
+                                            const Set<WPL> &C, int *list, uint32_t *cbuf,
+                                            int lane, ull &acc, ull &visits, ull &work) {
+    const int n = compact<WPL>(C, list, lane);
+    store_set<WPL>(cbuf, C, lane);
+    __syncwarp();
+    visits += ull(popc_set<WPL>(C));
+    for (int base = 0; base < n; base += 32) {
+        const int i = base + lane;
+        if (i >= n) break;
+        const int v = list[i];
+        const uint32_t *rv = rows + v * RS;
+        ull a = 0, x_seen = 0;
+        if (W == 1) {
+            const uint32_t cm = cbuf[0] & rv[0];
+            uint32_t m = cm;
+            x_seen = __popc(m);
+            while (m) {
+                const int x = __ffs(m) - 1;
+                m &= m - 1u;
+                a += __popc(cm & rows[x * RS]);
+            }
+        } else if (WPL == 1) {
+            // word-sparse: only words where C & row v is nonzero matter
+            uint32_t nzm = 0;
+            for (int w = 0; w < W; ++w) nzm |= (cbuf[w] & rv[w]) ? (1u << w) : 0u;
+            uint32_t ws = nzm;
+            while (ws) {
+                const int w = __ffs(ws) - 1;
+                ws &= ws - 1u;
+                uint32_t m = cbuf[w] & rv[w];
+                x_seen += __popc(m);
+                while (m) {
+                    const int x = (w << 5) + __ffs(m) - 1;
+                    m &= m - 1u;
+                    const uint32_t *rx = rows + x * RS;
+                    uint32_t w2s = nzm;
+                    int c = 0;
+                    while (w2s) {
+                        const int w2 = __ffs(w2s) - 1;
+                        w2s &= w2s - 1u;
+                        c += __popc(cbuf[w2] & rv[w2] & rx[w2]);
+                    }
+                    a += c;
+                }
+            }
+        } else {
+            for (int w = 0; w < W; ++w) {
+                uint32_t m = cbuf[w] & rv[w];
+                x_seen += __popc(m);
+                while (m) {
+                    const int x = (w << 5) + __ffs(m) - 1;
+                    m &= m - 1u;
+                    const uint32_t *rx = rows + x * RS;
+                    int c = 0;
+                    for (int w2 = 0; w2 < W; ++w2) c += __popc(cbuf[w2] & rv[w2] & rx[w2]);
+                    a += c;
+                }
+            }
+        }
+        acc += a;
+        visits += x_seen;
+        work += ull(W) * (1 + x_seen);
+    }
+    __syncwarp();
+}
+
 // argmax over v in C of popc(C & row v), lowest v on ties (engine_pivot.py:82-101)
 template <int WPL>
 __device__ __forceinline__ int select_pivot(const uint32_t *__restrict__ rows, int RS,
@@ -185,6 +272,175 @@ __device__ __forceinline__ int select_pivot(const uint32_t *__restrict__ rows, i
 }
 
 // ---------------------------------------------------------------------------
+// S-tier: sets of at most 32 members.  Once a candidate set X is that small,
+// its members are relabelled 0..n-1 in ascending local id (order, and hence
+// every tie-break, is preserved) and the induced rows are compressed to one
+// 32-bit word each (srow[i], per-warp shared memory; lane i also keeps its
+// own row in a register).  The rest of the subtree then runs on uniform
+// 32-bit scalars: next vertex = __ffs, child = one AND, pivot choice = one
+// POPC per lane + __reduce_max_sync, last two orientation levels = per-lane
+// bit loops.  The reference's visit order and counts are unchanged.
+// ---------------------------------------------------------------------------
+template <int WPL>
+__device__ __forceinline__ int warp_count(const Set<WPL> &X) {
+    return int(__reduce_add_sync(FULL, unsigned(popc_set<WPL>(X))));
+}
+
+// compress X (|X| <= 32) into srow; returns n; lane i (< n) row in *myrow
+template <int WPL>
+__device__ __forceinline__ int compress(const uint32_t *__restrict__ rows, int RS,
+                                        const Set<WPL> &X, int *list, uint32_t *srow, int lane,
+                                        uint32_t &myrow) {
+    const int n = compact<WPL>(X, list, lane);
+    uint32_t r = 0;
+    if (lane < n) {
+        const uint32_t *rc = rows + list[lane] * RS;
+        for (int j = 0; j < n; ++j) {
+            const int cj = list[j];
+            r |= ((rc[cj >> 5] >> (cj & 31)) & 1u) << j;
+        }
+    }
+    srow[lane] = r;
+    myrow = r;
+    __syncwarp();
+    return n;
+}
+
+// orientation, last two levels over compressed set C (C = frame last-1)
+__device__ __forceinline__ void pairs_small(const uint32_t *srow, uint32_t C, int lane, ull &acc,
+                                            ull &visits, ull &work) {
+    if ((C >> lane) & 1u) {
+        const uint32_t cm = C & srow[lane];
+        uint32_t m = cm;
+        const int xs = __popc(m);
+        visits += ull(1 + xs);
+        work += ull(1 + xs);
+        ull a = 0;
+        while (m) {
+            const int x = __ffs(m) - 1;
+            m &= m - 1u;
+            a += __popc(cm & srow[x]);
+        }
+        acc += a;
+    }
+}
+
+// orientation walk of a compressed subtree; C is frame s (s <= last - 1)
+__device__ void orient_small(const uint32_t *srow, uint32_t C, int s, int last, uint32_t *sstk,
+                             int lane, ull &acc, ull &visits, ull &work) {
+    if (s == last - 1) {
+        pairs_small(srow, C, lane, acc, visits, work);
+        __syncwarp();
+        return;
+    }
+    const int s0 = s;
+    uint32_t R = C;
+    for (;;) {
+        if (R == 0) {
+            if (s == s0) break;
+            --s;
+            C = sstk[2 * (s - s0)];
+            R = sstk[2 * (s - s0) + 1];
+            continue;
+        }
+        const int v = __ffs(R) - 1;
+        R &= R - 1u;
+        if (lane == 0) {
+            ++visits;
+            ++work;
+        }
+        const uint32_t X = C & srow[v];
+        if (!X) continue;
+        if (s + 2 == last) {
+            pairs_small(srow, X, lane, acc, visits, work);
+            __syncwarp();
+            continue;
+        }
+        if (lane == 0) {
+            sstk[2 * (s - s0)] = C;
+            sstk[2 * (s - s0) + 1] = R;
+        }
+        __syncwarp();
+        ++s;
+        C = X;
+        R = X;
+    }
+}
+
+__device__ __forceinline__ int select_small(uint32_t C, uint32_t myrow, int lane) {
+    const unsigned key = ((C >> lane) & 1u) ? ((unsigned(__popc(C & myrow)) + 1u) << 5) |
+                                                  unsigned(31 - lane)
+                                            : 0u;
+    return 31 - int(__reduce_max_sync(FULL, key) & 31u);
+}
+
+struct PivotLeafSink {
+    ull *s_hist;   // shared triangular histogram for len < sh_hl
+    int sh_hl;
+    ull *g_hist;   // global L x L histogram
+    int L;
+    __device__ __forceinline__ void add(int len, int np) const {
+        if (len < sh_hl) atomicAdd(&s_hist[len * (len + 1) / 2 + np], 1ull);
+        else atomicAdd(&g_hist[int64_t(len) * L + np], 1ull);
+    }
+};
+
+// pivot walk of a compressed subtree rooted at a fresh child set C (frame s,
+// pivot count npv); frames: 5 words (C, P, piv, npv, R) per level
+template <typename Sink>
+__device__ void pivot_small(const uint32_t *srow, uint32_t myrow, uint32_t C, int s, int npv,
+                            int t, bool allk, uint32_t *sstk, const Sink &sink, int lane,
+                            ull &visits, ull &work) {
+    const int s0 = s;
+    int piv = select_small(C, myrow, lane);
+    uint32_t P = C & ~srow[piv];
+    uint32_t R = P;
+    work += lane == 0 ? ull(__popc(C)) : 0ull;
+    for (;;) {
+        if (R == 0) {
+            if (s == s0) break;
+            --s;
+            const uint32_t *f = sstk + 5 * (s - s0);
+            C = f[0];
+            P = f[1];
+            piv = int(f[2]);
+            npv = int(f[3]);
+            R = f[4];
+            continue;
+        }
+        const int v = __ffs(R) - 1;
+        R &= R - 1u;
+        const int np2 = npv + (v == piv ? 1 : 0);
+        if (!allk && s + 1 - t > np2) continue;
+        if (lane == 0) {
+            ++visits;
+            ++work;
+        }
+        const uint32_t X = C & srow[v] & ~(P & ((1u << v) - 1u));
+        if (X) {
+            if (lane == 0) {
+                uint32_t *f = sstk + 5 * (s - s0);
+                f[0] = C;
+                f[1] = P;
+                f[2] = uint32_t(piv);
+                f[3] = uint32_t(npv);
+                f[4] = R;
+            }
+            __syncwarp();
+            ++s;
+            npv = np2;
+            C = X;
+            piv = select_small(C, myrow, lane);
+            P = C & ~srow[piv];
+            R = P;
+            if (lane == 0) work += ull(__popc(C));
+        } else if (allk || s + 1 >= t) {
+            if (lane == 0) sink.add(s + 1, np2);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // frames
 // ---------------------------------------------------------------------------
 struct Frames {
@@ -197,27 +453,43 @@ struct Frames {
     }
 };
 
-template <int WPL>
-__device__ __forceinline__ void store_set(uint32_t *f, const Set<WPL> &S, int lane) {
-#pragma unroll
-    for (int p = 0; p < WPL; ++p) f[p * 32 + lane] = S.w[p];
-}
-template <int WPL>
-__device__ __forceinline__ Set<WPL> load_set(const uint32_t *f, int lane) {
-    Set<WPL> S;
-#pragma unroll
-    for (int p = 0; p < WPL; ++p) S.w[p] = f[p * 32 + lane];
-    return S;
-}
+// per-warp S-tier scratch: compressed rows and the scalar frame stack
+struct SmallScratch {
+    uint32_t *srow;  // 32 words
+    uint32_t *sstk;  // 5 words per level, kSmallDepth levels
+};
+constexpr int kSmallDepth = 36;
+constexpr int kSmallWords = 32 + 5 * kSmallDepth;
 
 // ---------------------------------------------------------------------------
 // orient: one level-1 subtree (engine_orient.py:32-79).  The caller expanded
 // root-level vertex u (and counted its visit); C = row(u) is frame 1.
 // last = t - 2 >= 1.  Orient frame layout: [C: 32*WPL][cursor].
 // ---------------------------------------------------------------------------
+// hand a set X at frame s (s <= last-1) to the S-tier if it has <= 32
+// members; returns false (nothing done) otherwise
+template <int WPL>
+__device__ __forceinline__ bool orient_try_small(const uint32_t *__restrict__ rows, int RS, int W,
+                                                 const Set<WPL> &X, int s, int last, int *list,
+                                                 const SmallScratch &S, int lane, ull &acc,
+                                                 ull &visits, ull &work) {
+    if (W == 1) {  // rows are already one word: identity relabelling
+        orient_small(rows, __shfl_sync(FULL, X.w[0], 0), s, last, S.sstk, lane, acc, visits,
+                     work);
+        return true;
+    }
+    if (warp_count<WPL>(X) > 32) return false;
+    uint32_t myrow;
+    const int n = compress<WPL>(rows, RS, X, list, S.srow, lane, myrow);
+    orient_small(S.srow, n == 32 ? FULL : ((1u << n) - 1u), s, last, S.sstk, lane, acc, visits,
+                 work);
+    return true;
+}
+
 template <int WPL>
 __device__ void orient_subtree(const uint32_t *__restrict__ rows, int RS, int W, int last, int u,
-                               const Frames &F, int *list, ull &acc, ull &visits, ull &work) {
+                               const Frames &F, int *list, uint32_t *cbuf, const SmallScratch &SS,
+                               ull &acc, ull &visits, ull &work) {
     const int lane = threadIdx.x & 31;
     Set<WPL> C = load_row<WPL>(rows, RS, W, u, lane);
     if (last == 1) {  // frame 1 is the last level
@@ -226,6 +498,11 @@ __device__ void orient_subtree(const uint32_t *__restrict__ rows, int RS, int W,
         return;
     }
     if (!any_set<WPL>(C)) return;
+    if (orient_try_small<WPL>(rows, RS, W, C, 1, last, list, SS, lane, acc, visits, work)) return;
+    if (last == 2) {  // frame 1 is the next-to-last level
+        score_pairs<WPL>(rows, RS, W, C, list, cbuf, lane, acc, visits, work);
+        return;
+    }
     int s = 1;
     Set<WPL> R = C;
     store_set<WPL>(F.at(1), C, lane);
@@ -252,12 +529,13 @@ __device__ void orient_subtree(const uint32_t *__restrict__ rows, int RS, int W,
             const int w = p * 32 + lane;
             X.w[p] = w < W ? (C.w[p] & rv[w]) : 0u;
         }
-        if (s + 1 == last) {
-            visits += ull(popc_set<WPL>(X));
-            score_sum<WPL>(rows, RS, X, list, lane, acc, work, W);
+        if (!any_set<WPL>(X)) continue;
+        if (orient_try_small<WPL>(rows, RS, W, X, s + 1, last, list, SS, lane, acc, visits, work))
+            continue;
+        if (s + 2 == last) {  // X is the next-to-last frame
+            score_pairs<WPL>(rows, RS, W, X, list, cbuf, lane, acc, visits, work);
             continue;
         }
-        if (!any_set<WPL>(X)) continue;
         uint32_t *f = F.at(s);
         if (lane == 0) f[cur] = uint32_t(v);
         ++s;
@@ -274,22 +552,34 @@ __device__ void orient_subtree(const uint32_t *__restrict__ rows, int RS, int W,
 // Leaves are binned as hist[(path length, pivots)] (expanded exactly on the
 // host).  t: target; allk: no stopping rule.
 // ---------------------------------------------------------------------------
-struct PivotLeafSink {
-    ull *s_hist;   // shared triangular histogram for len < sh_hl
-    int sh_hl;
-    ull *g_hist;   // global L x L histogram
-    int L;
-    __device__ __forceinline__ void add(int len, int np) const {
-        if (len < sh_hl) atomicAdd(&s_hist[len * (len + 1) / 2 + np], 1ull);
-        else atomicAdd(&g_hist[int64_t(len) * L + np], 1ull);
+
+// hand a fresh child set X (frame s, pivot count npv) to the S-tier if it
+// has <= 32 members
+template <int WPL>
+__device__ __forceinline__ bool pivot_try_small(const uint32_t *__restrict__ rows, int RS, int W,
+                                                const Set<WPL> &X, int s, int npv, int t,
+                                                bool allk, int *list, const SmallScratch &S,
+                                                const PivotLeafSink &sink, int lane, ull &visits,
+                                                ull &work) {
+    if (W == 1) {  // rows are already one word: identity relabelling
+        const uint32_t c = __shfl_sync(FULL, X.w[0], 0);
+        const uint32_t myrow = ((c >> lane) & 1u) ? rows[lane * RS] : 0u;
+        pivot_small(rows, myrow, c, s, npv, t, allk, S.sstk, sink, lane, visits, work);
+        return true;
     }
-};
+    if (warp_count<WPL>(X) > 32) return false;
+    uint32_t myrow;
+    const int n = compress<WPL>(rows, RS, X, list, S.srow, lane, myrow);
+    pivot_small(S.srow, myrow, n == 32 ? FULL : ((1u << n) - 1u), s, npv, t, allk, S.sstk, sink,
+                lane, visits, work);
+    return true;
+}
 
 template <int WPL>
 __device__ void pivot_subtree(const uint32_t *__restrict__ rows, int RS, int W, int t, bool allk,
                               int v0, int piv0, const uint32_t *S0, const uint32_t *P0,
-                              const Frames &F, int *list, const PivotLeafSink &sink, ull &visits,
-                              ull &work) {
+                              const Frames &F, int *list, const SmallScratch &SS,
+                              const PivotLeafSink &sink, ull &visits, ull &work) {
     const int lane = threadIdx.x & 31;
     const int np0 = v0 == piv0 ? 1 : 0;
     if (!allk && 1 - t > np0) return;  // engine_pivot.py:152-153
@@ -310,6 +600,8 @@ __device__ void pivot_subtree(const uint32_t *__restrict__ rows, int RS, int W, 
         if ((allk || 1 >= t) && lane == 0) sink.add(1, np0);
         return;
     }
+    if (pivot_try_small<WPL>(rows, RS, W, C, 1, np0, t, allk, list, SS, sink, lane, visits, work))
+        return;
     const int PO = 32 * WPL, SC = 64 * WPL;  // P offset, scalars offset
     int s = 1;
     int npv = np0;
@@ -359,6 +651,9 @@ __device__ void pivot_subtree(const uint32_t *__restrict__ rows, int RS, int W, 
             X.w[p] = w < W ? (C.w[p] & rv[w] & ~(P.w[p] & below_mask(w, v))) : 0u;
         }
         if (any_set<WPL>(X)) {
+            if (pivot_try_small<WPL>(rows, RS, W, X, s + 1, np2, t, allk, list, SS, sink, lane,
+                                     visits, work))
+                continue;
             if (lane == 0) F.at(s)[SC + 2] = uint32_t(v);
             ++s;
             npv = np2;
