@@ -971,21 +971,21 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
         // concurrently (it fills SMs as the big-task CTAs retire)
         const int64_t n_small = n_tasks - n_big;
         CountParams q = p;
+        if (n_big > 0 && n_small > 0) {
+            if (!g->aux) KC_CUDA(cudaStreamCreateWithFlags(&g->aux, cudaStreamNonBlocking));
+            KC_CUDA(cudaEventRecord(e_fork, g->stream));
+            KC_CUDA(cudaStreamWaitEvent(g->aux, e_fork, 0));
+        }
         if (n_big > 0) {
             p.n_tasks = n_big;
             if (pivot) launch<MODE_PIVOT>(g, p, 0, keep, g->stream);
             else launch<MODE_ORIENT>(g, p, 0, keep, g->stream);
         }
         if (n_small > 0) {
-            if (!g->aux) KC_CUDA(cudaStreamCreateWithFlags(&g->aux, cudaStreamNonBlocking));
             q.tasks = tasks.as<int32_t>() + n_big;
             q.n_tasks = n_small;
             q.task_counter = o + 7;
             cudaStream_t st = n_big > 0 ? g->aux : g->stream;
-            if (n_big > 0) {
-                KC_CUDA(cudaEventRecord(e_fork, g->stream));
-                KC_CUDA(cudaStreamWaitEvent(g->aux, e_fork, 0));
-            }
             if (pivot) launch_warp<MODE_PIVOT>(g, q, keep, st);
             else launch_warp<MODE_ORIENT>(g, q, keep, st);
             if (n_big > 0) {

@@ -146,9 +146,15 @@ __global__ void k_orient_flags(const int32_t *__restrict__ col, const int32_t *_
 // K3 as ONE persistent cooperative kernel: the whole bulk-synchronous peel
 // runs on the device with grid-wide barriers (no host round trip per round).
 // order[] receives vertices in removal order; round r's frontier is the slice
-// [head, end) of it, and relax appends the next round's frontier at the tail.
-// ctl: [0] tail, [1]/[2] min live degree (alternating per scan), [3] degeneracy,
-//      [4] rounds.
+// [head, end) of it, and relax appends the next round's frontier at `tail`.
+//
+// Barrier discipline: the kernel is a sequence of steps separated by
+// grid.sync().  Step p appends through counter cnt[p%3] and reports a minimum
+// through mn[p%3]; every thread reads both right after the barrier ending
+// step p, and slot p%3 is only re-zeroed at the start of step p+2 (after the
+// barrier ending step p+1, which no thread passes before finishing its
+// reads).  All control values are therefore identical in every thread.
+// ctl: [0..2] cnt, [3..5] mn, [6] degeneracy, [7] rounds.
 __global__ void k_peel_coop(const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
                             int64_t n, int32_t *__restrict__ deg, int32_t *__restrict__ round_of,
                             int32_t *__restrict__ order, int32_t *ctl) {
@@ -158,23 +164,30 @@ __global__ void k_peel_coop(const int64_t *__restrict__ row_ptr, const int32_t *
     const int lane = threadIdx.x & 31;
     const int64_t gwarp = gtid >> 5, nwarps = gsz >> 5;
     const int32_t BIG = 0x7fffffff;
+    volatile int32_t *vctl = ctl;
+    int32_t *cnt = ctl, *mn = ctl + 3;
     for (int64_t v = gtid; v < n; v += gsz) {
         deg[v] = int32_t(row_ptr[v + 1] - row_ptr[v]);
         round_of[v] = -1;
     }
-    if (gtid == 0) {
-        ctl[0] = 0;
-        ctl[1] = BIG;
-        ctl[2] = BIG;
-    }
+    if (gtid == 0)
+        for (int i = 0; i < 3; ++i) {
+            cnt[i] = 0;
+            mn[i] = BIG;
+        }
     grid.sync();
-    volatile int32_t *vctl = ctl;
-    int64_t head = 0;
+    int p = 0;  // step index (uniform)
+    auto begin_step = [&]() {
+        if (gtid == 0) {
+            cnt[(p + 1) % 3] = 0;
+            mn[(p + 1) % 3] = BIG;
+        }
+    };
+    int64_t head = 0, tail = 0;
     int32_t level = 0, round = 0, degen = 0;
-    int scans = 0;
     while (head < n) {
-        // scan: live vertices of residual degree <= level start a level
-        const int mslot = 1 + (scans & 1);
+        // scan step: live vertices of residual degree <= level start a level
+        begin_step();
         for (int64_t base = gtid - lane; base < n; base += gsz) {
             const int64_t v = base + lane;
             const bool live = v < n && round_of[v] < 0;
@@ -182,47 +195,54 @@ __global__ void k_peel_coop(const int64_t *__restrict__ row_ptr, const int32_t *
             const bool take = live && d <= level;
             const unsigned mask = __ballot_sync(0xffffffffu, take);
             int off = 0;
-            if (lane == 0 && mask) off = atomicAdd(&ctl[0], __popc(mask));
+            if (lane == 0 && mask) off = atomicAdd(&cnt[p % 3], __popc(mask));
             off = __shfl_sync(0xffffffffu, off, 0);
-            if (take) order[off + __popc(mask & ((1u << lane) - 1))] = int32_t(v);
+            if (take) order[tail + off + __popc(mask & ((1u << lane) - 1))] = int32_t(v);
             int32_t dm = (live && !take) ? d : BIG;
             for (int o = 16; o; o >>= 1) dm = min(dm, __shfl_xor_sync(0xffffffffu, dm, o));
-            if (lane == 0 && dm != BIG) atomicMin(&ctl[mslot], dm);
+            if (lane == 0 && dm != BIG) atomicMin(&mn[p % 3], dm);
         }
-        // the other min slot was last read before the previous barrier
-        if (gtid == 0) ctl[1 + ((scans + 1) & 1)] = BIG;
         grid.sync();
-        int64_t end = vctl[0];
-        const int32_t mn = vctl[mslot];
-        ++scans;
-        if (end == head) {
-            level = mn;  // no live vertex at this level: jump to the next one
+        const int32_t added = vctl[p % 3];
+        const int32_t mnv = vctl[3 + p % 3];
+        ++p;
+        if (added == 0) {
+            level = mnv;  // no live vertex at this level: jump to the next one
             continue;
         }
+        int64_t end = tail + added;
+        tail = end;
         degen = level > degen ? level : degen;
         while (end > head) {
+            // mark step
+            begin_step();
             for (int64_t i = head + gtid; i < end; i += gsz) round_of[order[i]] = round;
             grid.sync();
-            // warp per frontier vertex: decrement live neighbours; one that
-            // crosses level+1 -> level joins the next round's frontier
+            ++p;
+            // relax step: warp per frontier vertex decrements live neighbours;
+            // one that crosses level+1 -> level joins the next round's frontier
+            begin_step();
             for (int64_t i = head + gwarp; i < end; i += nwarps) {
                 const int32_t v = order[i];
                 for (int64_t e = row_ptr[v] + lane; e < row_ptr[v + 1]; e += 32) {
                     const int32_t w = col[e];
                     if (round_of[w] >= 0) continue;
                     const int32_t old = atomicSub(&deg[w], 1);
-                    if (old == level + 1) order[atomicAdd(&ctl[0], 1)] = w;
+                    if (old == level + 1) order[tail + atomicAdd(&cnt[p % 3], 1)] = w;
                 }
             }
             grid.sync();
+            const int32_t nxt = vctl[p % 3];
+            ++p;
             head = end;
-            end = vctl[0];
+            end = tail + nxt;
+            tail = end;
             ++round;
         }
     }
     if (gtid == 0) {
-        ctl[3] = degen;
-        ctl[4] = round;
+        ctl[6] = degen;
+        ctl[7] = round;
     }
 }
 
@@ -435,7 +455,7 @@ static void degeneracy_rank(kc_graph *g, int64_t *degeneracy, int64_t *rounds_ou
     int32_t h[8] = {0};
     KC_CUDA(cudaMemcpyAsync(h, ctl, sizeof(h), cudaMemcpyDeviceToHost, g->stream));
     KC_CUDA(cudaStreamSynchronize(g->stream));
-    const int32_t round = h[4];
+    const int32_t round = h[7];
     // rank = position in (round, id) order
     int bits = kc_bits_for(n - 1 > 0 ? n - 1 : 1);
     int rbits = kc_bits_for(round > 0 ? round : 1);
@@ -453,7 +473,7 @@ static void degeneracy_rank(kc_graph *g, int64_t *degeneracy, int64_t *rounds_ou
     kc_free(round_of, g->stream);
     kc_free(order, g->stream);
     kc_free(ctl, g->stream);
-    *degeneracy = h[3];
+    *degeneracy = h[6];
     *rounds_out = round;
 }
 

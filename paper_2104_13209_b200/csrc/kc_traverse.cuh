@@ -71,6 +71,14 @@ __device__ __forceinline__ bool any_set(const Set<WPL> &s) {
     return __ballot_sync(FULL, x != 0) != 0;
 }
 
+// keep only local id v in R (lane-distributed)
+template <int WPL>
+__device__ __forceinline__ void restrict_to(Set<WPL> &R, int v, int lane) {
+#pragma unroll
+    for (int p = 0; p < WPL; ++p)
+        R.w[p] &= (p * 32 + lane == (v >> 5)) ? (1u << (v & 31)) : 0u;
+}
+
 template <int WPL>
 __device__ __forceinline__ int popc_set(const Set<WPL> &s) {  // per-lane part
     int c = 0;
@@ -394,7 +402,9 @@ __device__ void pivot_small(const uint32_t *srow, uint32_t myrow, uint32_t C, in
     const int s0 = s;
     int piv = select_small(C, myrow, lane);
     uint32_t P = C & ~srow[piv];
-    uint32_t R = P;
+    // engine_pivot.py:152-153 prunes branch v iff s+1-t > npv + [v == piv]:
+    // a frame with deficit npv+1 can only branch on its pivot (always in P)
+    uint32_t R = (!allk && s + 1 - t > npv) ? (P & (1u << piv)) : P;
     work += lane == 0 ? ull(__popc(C)) : 0ull;
     for (;;) {
         if (R == 0) {
@@ -418,6 +428,9 @@ __device__ void pivot_small(const uint32_t *srow, uint32_t myrow, uint32_t C, in
         }
         const uint32_t X = C & srow[v] & ~(P & ((1u << v) - 1u));
         if (X) {
+            // a child whose every branch would be pruned adds neither visits
+            // nor leaves: do not build it
+            if (!allk && s + 2 - t > np2 + 1) continue;
             if (lane == 0) {
                 uint32_t *f = sstk + 5 * (s - s0);
                 f[0] = C;
@@ -432,7 +445,7 @@ __device__ void pivot_small(const uint32_t *srow, uint32_t myrow, uint32_t C, in
             C = X;
             piv = select_small(C, myrow, lane);
             P = C & ~srow[piv];
-            R = P;
+            R = (!allk && s + 1 - t > npv) ? (P & (1u << piv)) : P;
             if (lane == 0) work += ull(__popc(C));
         } else if (allk || s + 1 >= t) {
             if (lane == 0) sink.add(s + 1, np2);
@@ -600,6 +613,7 @@ __device__ void pivot_subtree(const uint32_t *__restrict__ rows, int RS, int W, 
         if ((allk || 1 >= t) && lane == 0) sink.add(1, np0);
         return;
     }
+    if (!allk && 2 - t > np0 + 1) return;  // dead child
     if (pivot_try_small<WPL>(rows, RS, W, C, 1, np0, t, allk, list, SS, sink, lane, visits, work))
         return;
     const int PO = 32 * WPL, SC = 64 * WPL;  // P offset, scalars offset
@@ -613,6 +627,7 @@ __device__ void pivot_subtree(const uint32_t *__restrict__ rows, int RS, int W, 
         for (int p = 0; p < WPL; ++p) P.w[p] = C.w[p] & ~rp.w[p];
     }
     Set<WPL> R = P;
+    if (!allk && 2 - t > npv) restrict_to(R, piv, lane);
     {
         uint32_t *f = F.at(1);
         store_set<WPL>(f, C, lane);
@@ -634,6 +649,7 @@ __device__ void pivot_subtree(const uint32_t *__restrict__ rows, int RS, int W, 
             const int c = int(f[SC + 2]);
 #pragma unroll
             for (int p = 0; p < WPL; ++p) R.w[p] = P.w[p] & above_mask(p * 32 + lane, c);
+            if (!allk && s + 1 - t > npv) restrict_to(R, piv, lane);
             continue;
         }
         const int np2 = npv + (v == piv ? 1 : 0);
@@ -651,6 +667,7 @@ __device__ void pivot_subtree(const uint32_t *__restrict__ rows, int RS, int W, 
             X.w[p] = w < W ? (C.w[p] & rv[w] & ~(P.w[p] & below_mask(w, v))) : 0u;
         }
         if (any_set<WPL>(X)) {
+            if (!allk && s + 2 - t > np2 + 1) continue;  // dead child (see pivot_small)
             if (pivot_try_small<WPL>(rows, RS, W, X, s + 1, np2, t, allk, list, SS, sink, lane,
                                      visits, work))
                 continue;
@@ -663,6 +680,7 @@ __device__ void pivot_subtree(const uint32_t *__restrict__ rows, int RS, int W, 
 #pragma unroll
             for (int p = 0; p < WPL; ++p) P.w[p] = C.w[p] & ~rp.w[p];
             R = P;
+            if (!allk && s + 1 - t > npv) restrict_to(R, piv, lane);
             uint32_t *f = F.at(s);
             store_set<WPL>(f, C, lane);
             store_set<WPL>(f + PO, P, lane);
