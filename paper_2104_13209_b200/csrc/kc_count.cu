@@ -44,6 +44,9 @@ struct CountParams {
     int scheme;        // KC_SCHEME_*
     int t;             // target inside a task
     int all_k;         // pivot all-k
+    int split;         // tasks are out-edges of split vertex roots (see kc_do_count)
+    int32_t *overflow;   // warp kernel: edge tasks with more than kWarpD locals
+    ull *overflow_n;
     int dcap;          // max locals per task
     int wcap;          // ceil(dcap / 32)
     int group_size;    // reserved (sub-warp group size; traversal is warp-granular)
@@ -334,10 +337,8 @@ __global__ void __launch_bounds__(BLOCK) k_count(CountParams p) {
     __shared__ ull s_key[NW];
     __shared__ ull s_red[4 * NW];
     const int tid = threadIdx.x, warp = tid >> 5;
-    // layout: [hist u64][l2g i32 dcap][rows u32][S0 P0][per warp: list dcap, frames]
-    const int hist_cells = MODE == MODE_PIVOT ? p.sh_hl * (p.sh_hl + 1) / 2 : 0;
-    ull *s_hist = reinterpret_cast<ull *>(smem);
-    int32_t *l2g = reinterpret_cast<int32_t *>(smem + 8 * hist_cells);
+    // layout: [l2g i32 dcap][rows u32][S0 P0][per warp: list, cbuf, S-tier, leaf hist, frames]
+    int32_t *l2g = reinterpret_cast<int32_t *>(smem);
     uint32_t *area = reinterpret_cast<uint32_t *>(l2g + ((p.dcap + 3) & ~3));
     uint32_t *rows;
     if (p.rows_in_smem) {
@@ -349,26 +350,27 @@ __global__ void __launch_bounds__(BLOCK) k_count(CountParams p) {
     int32_t *scratch = reinterpret_cast<int32_t *>(area);  // edge-scheme staging (pre-traversal)
     uint32_t *S0 = area, *P0 = area + 32 * WPL;
     if (MODE == MODE_PIVOT) area += 64 * WPL;
-    const int per_warp =
-        ((p.dcap + 3) & ~3) + 32 * WPL + kct::kSmallWords + p.nsm_frames * p.fw;
+    const int hist_cells = MODE == MODE_PIVOT ? kct::kLeafCells : 0;
+    const int per_warp = ((p.dcap + 3) & ~3) + 32 * WPL + kct::kSmallWords + hist_cells +
+                         p.nsm_frames * p.fw;
     int *list = reinterpret_cast<int *>(area + warp * per_warp);
     uint32_t *cbuf = area + warp * per_warp + ((p.dcap + 3) & ~3);
     kct::SmallScratch SS;
     SS.srow = cbuf + 32 * WPL;
     SS.sstk = SS.srow + 32;
+    uint32_t *whist = SS.srow + kct::kSmallWords;
     kct::Frames F;
-    F.sm = SS.srow + kct::kSmallWords;
+    F.sm = whist + hist_cells;
     F.nsm = p.nsm_frames;
     F.fw = p.fw;
     F.gm = p.frames_global ? p.frames_global + (int64_t(blockIdx.x) * NW + warp) * p.frames_slot
                            : nullptr;
     kct::PivotLeafSink sink;
-    sink.s_hist = s_hist;
-    sink.sh_hl = p.sh_hl;
+    sink.whist = whist;
     sink.g_hist = p.hist;
     sink.L = p.hist_dim;
 
-    for (int i = tid; i < hist_cells; i += BLOCK) s_hist[i] = 0;
+    for (int i = tid & 31; i < hist_cells; i += 32) whist[i] = 0;
     ull acc = 0, visits = 0, tasks = 0, work = 0, bytes = 0;
     const bool directed = MODE == MODE_ORIENT || (MODE == MODE_EXTRACT && p.directed_out);
     const int t = p.t;
@@ -401,7 +403,12 @@ __global__ void __launch_bounds__(BLOCK) k_count(CountParams p) {
             if (tid == 0) *p.extract_d = d;
             continue;
         }
-        if (MODE == MODE_PIVOT && p.all_k) {
+        if (p.split) {
+            // edge item (v,u) of a split vertex root v: u is a level-1 visit of
+            // v's tree and the item walks u's subtree whatever its size
+            if (tid == 0) ++visits;
+            if (d == 0) continue;
+        } else if (MODE == MODE_PIVOT && p.all_k) {
             if (d == 0) continue;  // scheduler.py:180-181
         } else if (d < t) {
             continue;  // scheduler.py:155-156
@@ -420,19 +427,7 @@ __global__ void __launch_bounds__(BLOCK) k_count(CountParams p) {
         }
     }
     __syncthreads();
-    if (MODE == MODE_PIVOT) {
-        for (int i = tid; i < hist_cells; i += BLOCK) {
-            ull x = s_hist[i];
-            if (x) {
-                // triangular index -> (len, np)
-                int len = int((sqrtf(8.0f * i + 1.0f) - 1.0f) * 0.5f);
-                while (len * (len + 1) / 2 > i) --len;
-                while ((len + 1) * (len + 2) / 2 <= i) ++len;
-                int np = i - len * (len + 1) / 2;
-                atomicAdd(&p.hist[int64_t(len) * p.hist_dim + np], x);
-            }
-        }
-    }
+    if (MODE == MODE_PIVOT) sink.flush(tid & 31);
     if (MODE != MODE_EXTRACT) flush_block<BLOCK>(p, acc, visits, tasks, work, bytes, s_red);
 }
 
@@ -443,6 +438,7 @@ __global__ void __launch_bounds__(BLOCK) k_count(CountParams p) {
 // in the S-tier (their rows already are one word).
 // ---------------------------------------------------------------------------
 constexpr int kWarpD = 128;
+constexpr int kSplitD = 32;  // orientation/vertex: roots above this are split into edge items
 
 __device__ __forceinline__ bool gl_contains(const int32_t *__restrict__ a, int n, int32_t x) {
     int lo = 0, hi = n;
@@ -479,11 +475,13 @@ __device__ int warp_build(const CountParams &p, int32_t task, int32_t *l2g, uint
             const int32_t x = i < la ? p.ocol[ab + i] : 0;
             const bool f = i < la && gl_contains(p.ocol + bb, lb, x);
             const unsigned m = __ballot_sync(kct::FULL, f);
-            if (f) l2g[d + __popc(m & ((1u << lane) - 1u))] = x;
+            const int at = d + __popc(m & ((1u << lane) - 1u));
+            if (f && at < kWarpD) l2g[at] = x;
             d += __popc(m);
         }
     }
     __syncwarp();
+    if (d > kWarpD) return d;  // caller defers the task to the CTA kernel
     if (!need_rows || d == 0) return d;
     const int W = (d + 31) >> 5, RS = row_stride(W);
     for (int i = lane; i < d * RS; i += 32) rows[i] = 0u;
@@ -515,11 +513,11 @@ __global__ void __launch_bounds__(BLOCK) k_count_warp(CountParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ ull s_red[4 * NW];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int hist_cells = MODE == MODE_PIVOT ? p.sh_hl * (p.sh_hl + 1) / 2 : 0;
-    ull *s_hist = reinterpret_cast<ull *>(smem);
-    // per warp: l2g[D] rows[D*RSD] list[D] S0[32] P0[32] cbuf[32] small frames
-    const int per_warp = D + D * RSD + D + 32 * 3 + kct::kSmallWords + p.nsm_frames * p.fw;
-    uint32_t *base = reinterpret_cast<uint32_t *>(smem + 8 * hist_cells) + warp * per_warp;
+    const int hist_cells = MODE == MODE_PIVOT ? kct::kLeafCells : 0;
+    // per warp: l2g[D] rows[D*RSD] list[D] S0[32] P0[32] cbuf[32] small leafhist frames
+    const int per_warp =
+        D + D * RSD + D + 32 * 3 + kct::kSmallWords + hist_cells + p.nsm_frames * p.fw;
+    uint32_t *base = reinterpret_cast<uint32_t *>(smem) + warp * per_warp;
     int32_t *l2g = reinterpret_cast<int32_t *>(base);
     uint32_t *rows = base + D;
     int *list = reinterpret_cast<int *>(rows + D * RSD);
@@ -529,19 +527,19 @@ __global__ void __launch_bounds__(BLOCK) k_count_warp(CountParams p) {
     kct::SmallScratch SS;
     SS.srow = cbuf + 32;
     SS.sstk = SS.srow + 32;
+    uint32_t *whist = SS.srow + kct::kSmallWords;
     kct::Frames F;
-    F.sm = SS.srow + kct::kSmallWords;
+    F.sm = whist + hist_cells;
     F.nsm = p.nsm_frames;
     F.fw = p.fw;
     F.gm = p.frames_global ? p.frames_global + (int64_t(blockIdx.x) * NW + warp) * p.frames_slot
                            : nullptr;
     kct::PivotLeafSink sink;
-    sink.s_hist = s_hist;
-    sink.sh_hl = p.sh_hl;
+    sink.whist = whist;
     sink.g_hist = p.hist;
     sink.L = p.hist_dim;
-    for (int i = tid; i < hist_cells; i += BLOCK) s_hist[i] = 0;
-    __syncthreads();
+    for (int i = lane; i < hist_cells; i += 32) whist[i] = 0;
+    __syncwarp();
 
     ull acc = 0, visits = 0, tasks = 0, work = 0, bytes = 0;
     const int t = p.t;
@@ -554,7 +552,14 @@ __global__ void __launch_bounds__(BLOCK) k_count_warp(CountParams p) {
         const int32_t task = p.tasks[i];
         const bool need_rows = MODE == MODE_PIVOT || t >= 2;
         const int d = warp_build(p, task, l2g, rows, need_rows, MODE == MODE_ORIENT, bytes);
-        if (allk) {
+        if (d > D) {  // edge task larger than the warp tier: CTA kernel, next launch
+            if (lane == 0) p.overflow[atomicAdd(p.overflow_n, 1ull)] = task;
+            continue;
+        }
+        if (p.split) {
+            if (lane == 0) ++visits;  // see k_count
+            if (d == 0) continue;
+        } else if (allk) {
             if (d == 0) continue;
         } else if (d < t) {
             continue;
@@ -615,19 +620,8 @@ __global__ void __launch_bounds__(BLOCK) k_count_warp(CountParams p) {
         }
         __syncwarp();
     }
+    if (MODE == MODE_PIVOT) sink.flush(lane);
     __syncthreads();
-    if (MODE == MODE_PIVOT) {
-        for (int i = tid; i < hist_cells; i += BLOCK) {
-            ull x = s_hist[i];
-            if (x) {
-                int len = int((sqrtf(8.0f * i + 1.0f) - 1.0f) * 0.5f);
-                while (len * (len + 1) / 2 > i) --len;
-                while ((len + 1) * (len + 2) / 2 <= i) ++len;
-                int np = i - len * (len + 1) / 2;
-                atomicAdd(&p.hist[int64_t(len) * p.hist_dim + np], x);
-            }
-        }
-    }
     flush_block<BLOCK>(p, acc, visits, tasks, work, bytes, s_red);
 }
 
@@ -655,13 +649,14 @@ __global__ void k_vertex_select(const int64_t *__restrict__ orow, const int32_t 
 
 __global__ void k_edge_select(const int64_t *__restrict__ orow, const int32_t *__restrict__ ocoo,
                               const int32_t *__restrict__ ocol, int64_t m, int64_t lo, int64_t hi,
-                              int min_d, uint8_t *__restrict__ keep, uint32_t *__restrict__ key) {
+                              int min_d, const uint8_t *__restrict__ vsel,
+                              uint8_t *__restrict__ keep, uint32_t *__restrict__ key) {
     for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < m;
          e += int64_t(gridDim.x) * blockDim.x) {
         int32_t u = ocoo[e], v = ocol[e];
         int64_t du = orow[u + 1] - orow[u], dv = orow[v + 1] - orow[v];
         int64_t b = du < dv ? du : dv;  // |N+(u) ∩ N+(v)| <= min
-        keep[e] = e >= lo && e < hi && b >= min_d;
+        keep[e] = e >= lo && e < hi && b >= min_d && (!vsel || vsel[u]);
         key[e] = uint32_t(b);  // bound on the task's locals: routes it to the warp/CTA kernel
     }
 }
@@ -676,6 +671,13 @@ __global__ void k_split_point(const uint32_t *__restrict__ keys, int64_t n, uint
         else hi = mid;
     }
     *out = int32_t(lo);
+}
+
+__global__ void k_mark_roots(const int32_t *__restrict__ roots, int64_t n,
+                             uint8_t *__restrict__ vsel) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x)
+        vsel[roots[i]] = 1;
 }
 
 __global__ void k_iota(int32_t *__restrict__ a, int64_t n) {
@@ -716,7 +718,7 @@ struct DevBuf {
 // order with enough locals, sorted by descending cost (largest first keeps the
 // persistent queue balanced).  Returns the count.
 int64_t build_tasks(kc_graph *g, int scheme, int64_t lo, int64_t hi, int min_d, DevBuf &out,
-                    uint32_t big_thr, int64_t *n_big) {
+                    uint32_t big_thr, int64_t *n_big, const uint8_t *vsel = nullptr) {
     const int64_t N = scheme == KC_SCHEME_EDGE ? g->m_dir : g->n;
     *n_big = 0;
     if (N == 0) return 0;
@@ -736,7 +738,7 @@ int64_t build_tasks(kc_graph *g, int scheme, int64_t lo, int64_t hi, int min_d, 
             key.as<uint32_t>());
     } else {
         k_edge_select<<<grid_1d(N, g->num_sms), 256, 0, g->stream>>>(
-            g->orow_ptr, g->ocoo, g->ocol, N, lo, hi, min_d, keep.as<uint8_t>(),
+            g->orow_ptr, g->ocoo, g->ocol, N, lo, hi, min_d, vsel, keep.as<uint8_t>(),
             key.as<uint32_t>());
     }
     k_iota<<<grid_1d(N, g->num_sms), 256, 0, g->stream>>>(ids.as<int32_t>(), N);
@@ -794,7 +796,7 @@ template <int MODE, int WPL>
 void launch_wpl(kc_graph *g, CountParams &p, int grid_override, Keep &keep,
                 cudaStream_t stream) {
     constexpr int NW = kBlock / 32;
-    const size_t hist_bytes = MODE == MODE_PIVOT ? 8 * size_t(p.sh_hl) * (p.sh_hl + 1) / 2 : 0;
+    const size_t hist_words = MODE == MODE_PIVOT ? kct::kLeafCells : 0;
     const size_t dpad = size_t((p.dcap + 3) & ~3);
     const size_t l2g_bytes = 4 * dpad;
     const size_t rows_words = (size_t(p.dcap) * row_stride(p.wcap) + 3) & ~size_t(3);
@@ -802,14 +804,15 @@ void launch_wpl(kc_graph *g, CountParams &p, int grid_override, Keep &keep,
     const int need = frames_needed(MODE, p.t, p.dcap);
     auto area_words = [&](int nsm) {
         size_t w = (MODE == MODE_PIVOT ? 64 * WPL : 0) +
-                   size_t(NW) * (dpad + 32 * WPL + kct::kSmallWords + size_t(nsm) * p.fw);
+                   size_t(NW) * (dpad + 32 * WPL + kct::kSmallWords + hist_words +
+                                 size_t(nsm) * p.fw);
         if (p.scheme == KC_SCHEME_EDGE) w = std::max(w, dpad);
         return w;
     };
     // as many shared frames as fit the target budget (at least 4, at most need)
     int nsm = std::min(need, 64);
     auto total = [&](int ns, bool rows_smem) {
-        return hist_bytes + l2g_bytes + 4 * area_words(ns) + (rows_smem ? 4 * rows_words : 0) + 64;
+        return l2g_bytes + 4 * area_words(ns) + (rows_smem ? 4 * rows_words : 0) + 64;
     };
     p.rows_in_smem = total(std::min(nsm, 4), true) <= size_t(kSmemMax);
     while (nsm > 4 && total(nsm, p.rows_in_smem) > size_t(kSmemTarget)) nsm >>= 1;
@@ -846,13 +849,13 @@ template <int MODE>
 void launch_warp(kc_graph *g, CountParams &p, Keep &keep, cudaStream_t stream) {
     constexpr int NW = kBlock / 32;
     constexpr int D = kWarpD, RSD = (kWarpD / 32) | 1;
-    const size_t hist_bytes = MODE == MODE_PIVOT ? 8 * size_t(p.sh_hl) * (p.sh_hl + 1) / 2 : 0;
+    const size_t hist_words = MODE == MODE_PIVOT ? kct::kLeafCells : 0;
     p.fw = MODE == MODE_PIVOT ? 64 + 4 : 32 + 4;
     const int need = std::max(1, std::min(frames_needed(MODE, p.t, D), D + 2));
-    const size_t fixed = size_t(D) + D * RSD + D + 96 + kct::kSmallWords;
+    const size_t fixed = size_t(D) + D * RSD + D + 96 + kct::kSmallWords + hist_words;
     int nsm = std::min(need, 8);
     p.nsm_frames = nsm;
-    const size_t smem = hist_bytes + 4 * size_t(NW) * (fixed + size_t(nsm) * p.fw) + 64;
+    const size_t smem = 4 * size_t(NW) * (fixed + size_t(nsm) * p.fw) + 64;
     auto kern = k_count_warp<kBlock, MODE>;
     KC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     int per_sm = 0;
@@ -924,12 +927,31 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
     int64_t hi = a->task_hi < 0 || a->task_hi > all ? all : a->task_hi;
     if (lo > hi) lo = hi;
     const int min_d = a->all_k ? 1 : (t > 1 ? t : 1);
+    // Orientation, vertex scheme, t >= 4: roots with more than kSplitD locals
+    // are split into their out-edge items (v,u) -- the level-1 subtrees of v's
+    // tree -- so a hub's tree spreads over the whole GPU instead of one CTA.
+    // Item (v,u) walks u's subtree over N+(v) n N+(u) with target t-1 (the
+    // edge scheme's sub-graph) and counts u's own visit, so counts and
+    // visits are exactly the vertex scheme's (engine_orient.py:32-79).
+    const bool split = !pivot && a->scheme == KC_SCHEME_VERTEX && t >= 4;
     DevBuf tasks;
     int64_t n_big = 0;
-    const int64_t n_tasks = build_tasks(g, a->scheme, lo, hi, min_d, tasks, kWarpD, &n_big);
+    const int64_t n_tasks =
+        build_tasks(g, a->scheme, lo, hi, min_d, tasks, split ? kSplitD : kWarpD, &n_big);
+    DevBuf items;
+    int64_t n_items = 0, n_items_big = 0;
+    if (split && n_big > 0) {
+        DevBuf vsel(size_t(g->n > 0 ? g->n : 1));
+        KC_CUDA(cudaMemsetAsync(vsel.p, 0, size_t(g->n > 0 ? g->n : 1), g->stream));
+        k_mark_roots<<<grid_1d(n_big, g->num_sms), 256, 0, g->stream>>>(tasks.as<int32_t>(), n_big,
+                                                                        vsel.as<uint8_t>());
+        KC_CUDA(cudaGetLastError());
+        n_items = build_tasks(g, KC_SCHEME_EDGE, 0, g->m_dir, 0, items, kWarpD, &n_items_big,
+                              vsel.as<uint8_t>());
+    }
 
-    DevBuf outs(8 * (10 + size_t(kSmidSlots)));
-    KC_CUDA(cudaMemsetAsync(outs.p, 0, 8 * (10 + size_t(kSmidSlots)), g->stream));
+    DevBuf outs(8 * (16 + size_t(kSmidSlots)));
+    KC_CUDA(cudaMemsetAsync(outs.p, 0, 8 * (16 + size_t(kSmidSlots)), g->stream));
     DevBuf dhist(pivot ? 8 * size_t(L * L) : 8);
     if (pivot) KC_CUDA(cudaMemsetAsync(dhist.p, 0, 8 * size_t(L * L), g->stream));
 
@@ -965,35 +987,75 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
     KC_CUDA(cudaEventCreateWithFlags(&e_join, cudaEventDisableTiming));
     KC_CUDA(cudaEventRecord(e0, g->stream));
     Keep keep;
-    if (n_tasks > 0) {
-        // big tasks (more than kWarpD locals): CTA-cooperative kernel on the
-        // graph stream; small tasks: warp-per-task kernel on the aux stream,
-        // concurrently (it fills SMs as the big-task CTAs retire)
-        const int64_t n_small = n_tasks - n_big;
-        CountParams q = p;
-        if (n_big > 0 && n_small > 0) {
-            if (!g->aux) KC_CUDA(cudaStreamCreateWithFlags(&g->aux, cudaStreamNonBlocking));
-            KC_CUDA(cudaEventRecord(e_fork, g->stream));
-            KC_CUDA(cudaStreamWaitEvent(g->aux, e_fork, 0));
+    // Edge tasks (and split items) all go to the warp-per-task kernel; the few
+    // whose intersection exceeds kWarpD locals are appended to an overflow
+    // list and run by the CTA-cooperative kernel afterwards.  Vertex tasks
+    // are routed exactly by out-degree: big ones to the CTA kernel on the
+    // graph stream, concurrently with the warp kernel on the aux stream.
+    const bool edge_like = split || a->scheme == KC_SCHEME_EDGE;
+    DevBuf ovf(4 * size_t(std::max<int64_t>(split ? n_items : n_tasks, 1)));
+    p.overflow = ovf.as<int32_t>();
+    p.overflow_n = o + 8 + kSmidSlots + 3;
+    if (!g->aux) KC_CUDA(cudaStreamCreateWithFlags(&g->aux, cudaStreamNonBlocking));
+    KC_CUDA(cudaEventRecord(e_fork, g->stream));
+    KC_CUDA(cudaStreamWaitEvent(g->aux, e_fork, 0));
+    if (split) {
+        if (n_items > 0) {
+            CountParams q = p;
+            q.scheme = KC_SCHEME_EDGE;
+            q.t = t - 1;
+            q.split = 1;
+            q.tasks = items.as<int32_t>();
+            q.n_tasks = n_items;
+            q.task_counter = o + 8 + kSmidSlots + 2;
+            launch_warp<MODE_ORIENT>(g, q, keep, g->stream);
         }
-        if (n_big > 0) {
-            p.n_tasks = n_big;
-            if (pivot) launch<MODE_PIVOT>(g, p, 0, keep, g->stream);
-            else launch<MODE_ORIENT>(g, p, 0, keep, g->stream);
-        }
-        if (n_small > 0) {
+        if (n_tasks - n_big > 0) {
+            CountParams q = p;
             q.tasks = tasks.as<int32_t>() + n_big;
-            q.n_tasks = n_small;
+            q.n_tasks = n_tasks - n_big;
+            launch_warp<MODE_ORIENT>(g, q, keep, g->aux);
+        }
+    } else if (a->scheme == KC_SCHEME_EDGE) {
+        if (n_tasks > 0) {
+            CountParams q = p;
+            if (pivot) launch_warp<MODE_PIVOT>(g, q, keep, g->stream);
+            else launch_warp<MODE_ORIENT>(g, q, keep, g->stream);
+        }
+    } else {
+        if (n_big > 0) {
+            CountParams b = p;
+            b.n_tasks = n_big;
+            if (pivot) launch<MODE_PIVOT>(g, b, 0, keep, g->stream);
+            else launch<MODE_ORIENT>(g, b, 0, keep, g->stream);
+        }
+        if (n_tasks - n_big > 0) {
+            CountParams q = p;
+            q.tasks = tasks.as<int32_t>() + n_big;
+            q.n_tasks = n_tasks - n_big;
             q.task_counter = o + 7;
-            cudaStream_t st = n_big > 0 ? g->aux : g->stream;
-            if (pivot) launch_warp<MODE_PIVOT>(g, q, keep, st);
-            else launch_warp<MODE_ORIENT>(g, q, keep, st);
-            if (n_big > 0) {
-                KC_CUDA(cudaEventRecord(e_join, g->aux));
-                KC_CUDA(cudaStreamWaitEvent(g->stream, e_join, 0));
-            }
+            if (pivot) launch_warp<MODE_PIVOT>(g, q, keep, g->aux);
+            else launch_warp<MODE_ORIENT>(g, q, keep, g->aux);
         }
     }
+    if (edge_like) {
+        ull n_ovf = 0;
+        KC_CUDA(cudaMemcpyAsync(&n_ovf, p.overflow_n, 8, cudaMemcpyDeviceToHost, g->stream));
+        KC_CUDA(cudaStreamSynchronize(g->stream));
+        if (n_ovf > 0) {
+            CountParams b = p;
+            b.scheme = KC_SCHEME_EDGE;
+            b.t = split ? t - 1 : t;
+            b.split = split ? 1 : 0;
+            b.tasks = ovf.as<int32_t>();
+            b.n_tasks = int64_t(n_ovf);
+            b.task_counter = o + 8 + kSmidSlots + 4;
+            if (pivot) launch<MODE_PIVOT>(g, b, 0, keep, g->stream);
+            else launch<MODE_ORIENT>(g, b, 0, keep, g->stream);
+        }
+    }
+    KC_CUDA(cudaEventRecord(e_join, g->aux));
+    KC_CUDA(cudaStreamWaitEvent(g->stream, e_join, 0));
     KC_CUDA(cudaEventRecord(e1, g->stream));
     KC_CUDA(cudaEventSynchronize(e1));
     float ms = 0;

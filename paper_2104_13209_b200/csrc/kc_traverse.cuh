@@ -382,14 +382,41 @@ __device__ __forceinline__ int select_small(uint32_t C, uint32_t myrow, int lane
     return 31 - int(__reduce_max_sync(FULL, key) & 31u);
 }
 
+// Pivot leaves are binned per (path length, pivot count).  Each warp owns a
+// u32 histogram for len < kLeafHL in shared memory, written by lane 0 only --
+// no atomics (64-bit shared atomicAdd is a CAS spin loop on sm_100) -- and
+// flushed to the global u64 L x L histogram at 2^31 and at kernel end.
+constexpr int kLeafHL = 32;
+constexpr int kLeafCells = kLeafHL * (kLeafHL + 1) / 2;
 struct PivotLeafSink {
-    ull *s_hist;   // shared triangular histogram for len < sh_hl
-    int sh_hl;
-    ull *g_hist;   // global L x L histogram
+    uint32_t *whist;  // this warp's kLeafCells counters
+    ull *g_hist;      // global L x L histogram
     int L;
     __device__ __forceinline__ void add(int len, int np) const {
-        if (len < sh_hl) atomicAdd(&s_hist[len * (len + 1) / 2 + np], 1ull);
-        else atomicAdd(&g_hist[int64_t(len) * L + np], 1ull);
+        if (len < kLeafHL) {
+            uint32_t &c = whist[len * (len + 1) / 2 + np];
+            if (++c == 0x80000000u) {
+                atomicAdd(&g_hist[int64_t(len) * L + np], 0x80000000ull);
+                c = 0;
+            }
+        } else {
+            atomicAdd(&g_hist[int64_t(len) * L + np], 1ull);
+        }
+    }
+    // whole warp: add the per-warp counters to the global histogram
+    __device__ __forceinline__ void flush(int lane) const {
+        __syncwarp();
+        for (int i = lane; i < kLeafCells; i += 32) {
+            const uint32_t x = whist[i];
+            if (!x) continue;
+            int len = int((sqrtf(8.0f * i + 1.0f) - 1.0f) * 0.5f);
+            while (len * (len + 1) / 2 > i) --len;
+            while ((len + 1) * (len + 2) / 2 <= i) ++len;
+            const int np = i - len * (len + 1) / 2;
+            atomicAdd(&g_hist[int64_t(len) * L + np], ull(x));
+            whist[i] = 0;
+        }
+        __syncwarp();
     }
 };
 
