@@ -33,7 +33,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, HERE)
 
 # BASELINE.json configs[1]: RMAT scale-18 ef16, degeneracy orientation, 1 GPU
-DEFAULTS = dict(workload="rmat18", k=4, algo="orient", scheme="vertex", criterion="degeneracy")
+DEFAULTS = dict(workload="rmat18", k=7, algo="auto", scheme="auto", criterion="degeneracy")
 METRIC = "k-cliques/sec"
 FLUSH_BYTES = 512 << 20  # > 126 MB L2
 
@@ -41,7 +41,7 @@ FLUSH_BYTES = 512 << 20  # > 126 MB L2
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--workload", default=DEFAULTS["workload"])
@@ -54,7 +54,17 @@ def parse():
                     help="target CPU seconds of the oracle baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    return ap.parse_args()
+    ap.add_argument("--per-k", default="4,7,10",
+                    help="also time these k (1 warm-up + 2 timed steps each) into per_k")
+    a = ap.parse_args()
+    from paper_2104_13209_b200.cli import b200_auto
+
+    auto_algo, auto_scheme = b200_auto(a.k)
+    if a.algo == "auto":
+        a.algo = auto_algo
+    if a.scheme == "auto":
+        a.scheme = auto_scheme
+    return a
 
 
 def workload_edges(name):
@@ -157,7 +167,9 @@ def count_kernel_launches(step):
         for ev in prof.events():
             if ev.device_type.name == "CUDA" and not ev.name.startswith("Memcpy") \
                     and not ev.name.startswith("Memset"):
-                names[ev.name] = names.get(ev.name, 0) + 1
+                nm = ev.name.split("(")[0].replace("(anonymous namespace)::", "")
+                nm = nm.replace("void ", "").split("<")[0][-60:]
+                names[nm] = names.get(nm, 0) + 1
         return sum(names.values()), names
     except Exception as exc:  # profiler unavailable: report unknown
         return None, {"error": str(exc)[:200]}
@@ -200,6 +212,27 @@ def run_ours(a):
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
+
+    def time_steps(fn, n):
+        """n steps timed with events on the library stream, L2 flushed between."""
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(n)]
+        r = None
+        barrier()
+        for i in range(n):
+            flush.fill_(i)
+            torch.cuda.synchronize()
+            evs[i][0].record(stream)
+            r = fn()
+            evs[i][1].record(stream)
+            torch.cuda.synchronize()
+        barrier()
+        tot = float(sum(s0.elapsed_time(s1) for s0, s1 in evs))
+        if world > 1:
+            tt = torch.tensor([tot], dtype=torch.float64, device=f"cuda:{local}")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            tot = float(tt.item())
+        return r, tot
 
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
@@ -255,6 +288,29 @@ def run_ours(a):
                "ms_per_step": e_ms / a.steps, "h2d_bytes_per_step": int(edges.nbytes),
                "d2h_bytes_per_step": int(d2h), "timer": "host wall clock, synced"}
 
+    # the other k of the metric (BASELINE.json: k=4/7/10), auto algorithm per k
+    per_k = {}
+    from paper_2104_13209_b200.cli import b200_auto
+
+    for kk in [int(x) for x in a.per_k.split(",") if x.strip()]:
+        if kk == a.k:
+            per_k[str(kk)] = {"algorithm": a.algo, "scheme": a.scheme, "count": str(count),
+                              "ms_per_step": total_ms / a.steps, "cliques_per_s": value}
+            continue
+        al, sc = b200_auto(kk)
+        c2 = kc.RunConfig(k=kk, algorithm=al, scheme=sc, criterion=a.criterion)
+
+        def st(c2=c2):
+            if world > 1:
+                return run_count_sharded(g, c2, rank, world)
+            return kc.run_count(g, c2)
+
+        st()
+        r2, t2 = time_steps(st, 2)
+        per_k[str(kk)] = {"algorithm": al, "scheme": sc, "count": str(r2.count),
+                          "ms_per_step": t2 / 2, "cliques_per_s": r2.count * 2 / (t2 / 1e3),
+                          "visits": r2.load.total}
+
     roof = roofline(kc, g, cfg, rep, a, local) if rank == 0 else None
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
@@ -272,7 +328,7 @@ def run_ours(a):
             "clocks": clk.summary(), "e2e": e2e, "gpu_launches": (n_launch * a.steps
                                                                   if n_launch else None),
             "gpu_launches_per_step": n_launch, "kernels": launch_names,
-            "roofline": roof, "cpu_baseline": cpu,
+            "roofline": roof, "cpu_baseline": cpu, "per_k": per_k,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -252,7 +252,7 @@ __device__ void orient_task(const CountParams &p, const uint32_t *rows, int d,
             for (int w = 0; w < W; ++w) c += __popc(ru[w]);
             acc += ull(c);
             ++visits;
-            work += ull(W);
+            work += 1;
         }
         return;
     }
@@ -264,7 +264,7 @@ __device__ void orient_task(const CountParams &p, const uint32_t *rows, int d,
         if (u >= d) break;
         if (lane == 0) {
             ++visits;
-            work += ull(W);
+            work += 1;
         }
         kct::orient_subtree<WPL>(rows, RS, W, last, u, F, list, cbuf, SS, acc, visits, work);
     }
@@ -276,7 +276,8 @@ __device__ void orient_task(const CountParams &p, const uint32_t *rows, int d,
 template <int BLOCK, int WPL>
 __device__ void pivot_task(const CountParams &p, const uint32_t *rows, int d, uint32_t *S0,
                            uint32_t *P0, const kct::Frames &F, int *list,
-                           const kct::SmallScratch &SS, const kct::PivotLeafSink &sink, int *s_next, int *s_piv0, ull *s_key,
+                           const kct::SmallScratch &SS, const kct::PivotLeafSink &sink,
+                           const kct::StealStack &q, int *s_next, int *s_piv0, ull *s_key,
                            ull &visits, ull &work) {
     constexpr int NW = BLOCK / 32;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -305,12 +306,17 @@ __device__ void pivot_task(const CountParams &p, const uint32_t *rows, int d, ui
         ull b = 0;
         for (int w = 0; w < NW; ++w) b = s_key[w] > b ? s_key[w] : b;
         *s_piv0 = int(0xffffffffu - uint32_t(b & 0xffffffffull));
-        work += ull(d) * W;
+        work += ull(d);
     }
     __syncthreads();
     const int piv0 = *s_piv0;
     const uint32_t *rp0 = rows + piv0 * RS;
     for (int w = tid; w < 32 * WPL; w += BLOCK) P0[w] = w < W ? (S0[w] & ~rp0[w]) : 0u;
+    if (tid == 0) {
+        *q.lock = 0;
+        *q.size = 0;
+        *q.idle = 0;
+    }
     __syncthreads();
     for (;;) {
         int v = 0;
@@ -319,14 +325,16 @@ __device__ void pivot_task(const CountParams &p, const uint32_t *rows, int d, ui
         if (v >= d) break;
         if (!((P0[v >> 5] >> (v & 31)) & 1u)) continue;
         kct::pivot_subtree<WPL>(rows, RS, W, p.t, p.all_k != 0, v, piv0, S0, P0, F, list, SS,
-                                sink, visits, work);
+                                sink, visits, work, &q);
     }
+    kct::pivot_steal_loop<WPL>(rows, RS, W, p.t, p.all_k != 0, F, list, SS, sink, q, visits, work);
 }
 
 // ---------------------------------------------------------------------------
 // the persistent kernel
 // ---------------------------------------------------------------------------
 enum Mode { MODE_ORIENT = 0, MODE_PIVOT = 1, MODE_EXTRACT = 2 };
+constexpr int kStealCap = 16;  // pivot work-sharing stack slots per CTA
 
 template <int BLOCK, int MODE, int WPL>
 __global__ void __launch_bounds__(BLOCK) k_count(CountParams p) {
@@ -349,7 +357,16 @@ __global__ void __launch_bounds__(BLOCK) k_count(CountParams p) {
     }
     int32_t *scratch = reinterpret_cast<int32_t *>(area);  // edge-scheme staging (pre-traversal)
     uint32_t *S0 = area, *P0 = area + 32 * WPL;
-    if (MODE == MODE_PIVOT) area += 64 * WPL;
+    kct::StealStack q;
+    __shared__ int s_q[3];
+    q.lock = s_q;
+    q.size = s_q + 1;
+    q.idle = s_q + 2;
+    q.cap = kStealCap;
+    q.iw = 32 * WPL + 4;
+    q.nwarps = NW;
+    q.items = area + 64 * WPL;
+    if (MODE == MODE_PIVOT) area += 64 * WPL + kStealCap * (32 * WPL + 4);
     const int hist_cells = MODE == MODE_PIVOT ? kct::kLeafCells : 0;
     const int per_warp = ((p.dcap + 3) & ~3) + 32 * WPL + kct::kSmallWords + hist_cells +
                          p.nsm_frames * p.fw;
@@ -419,12 +436,14 @@ __global__ void __launch_bounds__(BLOCK) k_count(CountParams p) {
             if (tid == 0) acc += t == 0 ? 1ull : ull(d);
             continue;
         }
+        const ull wt0 = work;  // units -> §8(d) word-ops of this task below
         if (MODE == MODE_ORIENT) {
             orient_task<BLOCK, WPL>(p, rows, d, F, list, cbuf, SS, &s_next, acc, visits, work);
         } else {
-            pivot_task<BLOCK, WPL>(p, rows, d, S0, P0, F, list, SS, sink, &s_next, &s_piv0, s_key,
-                                   visits, work);
+            pivot_task<BLOCK, WPL>(p, rows, d, S0, P0, F, list, SS, sink, q, &s_next, &s_piv0,
+                                   s_key, visits, work);
         }
+        work = wt0 + (work - wt0) * ull((d + 31) >> 5);
     }
     __syncthreads();
     if (MODE == MODE_PIVOT) sink.flush(tid & 31);
@@ -571,6 +590,7 @@ __global__ void __launch_bounds__(BLOCK) k_count_warp(CountParams p) {
         }
         const int W = (d + 31) >> 5, RS = row_stride(W);
         const uint32_t all = d >= 32 ? kct::FULL : ((1u << d) - 1u);
+        const ull wt0 = work;  // units -> §8(d) word-ops of this task at the end
         if (MODE == MODE_ORIENT) {
             const int last = t - 2;
             if (last == 0) {
@@ -580,7 +600,7 @@ __global__ void __launch_bounds__(BLOCK) k_count_warp(CountParams p) {
                     for (int w = 0; w < W; ++w) c += __popc(ru[w]);
                     acc += ull(c);
                     ++visits;
-                    work += ull(W);
+                    work += 1;
                 }
             } else if (W == 1) {
                 kct::orient_small(rows, all, 0, last, SS.sstk, lane, acc, visits, work);
@@ -588,7 +608,7 @@ __global__ void __launch_bounds__(BLOCK) k_count_warp(CountParams p) {
                 for (int u = 0; u < d; ++u) {
                     if (lane == 0) {
                         ++visits;
-                        work += ull(W);
+                        work += 1;
                     }
                     kct::orient_subtree<WPL>(rows, RS, W, last, u, F, list, cbuf, SS, acc, visits,
                                              work);
@@ -618,6 +638,7 @@ __global__ void __launch_bounds__(BLOCK) k_count_warp(CountParams p) {
                 }
             }
         }
+        work = wt0 + (work - wt0) * ull(W);
         __syncwarp();
     }
     if (MODE == MODE_PIVOT) sink.flush(lane);
@@ -650,12 +671,14 @@ __global__ void k_vertex_select(const int64_t *__restrict__ orow, const int32_t 
 __global__ void k_edge_select(const int64_t *__restrict__ orow, const int32_t *__restrict__ ocoo,
                               const int32_t *__restrict__ ocol, int64_t m, int64_t lo, int64_t hi,
                               int min_d, const uint8_t *__restrict__ vsel,
-                              uint8_t *__restrict__ keep, uint32_t *__restrict__ key) {
+                              const int32_t *__restrict__ esize, uint8_t *__restrict__ keep,
+                              uint32_t *__restrict__ key) {
     for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < m;
          e += int64_t(gridDim.x) * blockDim.x) {
         int32_t u = ocoo[e], v = ocol[e];
         int64_t du = orow[u + 1] - orow[u], dv = orow[v + 1] - orow[v];
-        int64_t b = du < dv ? du : dv;  // |N+(u) ∩ N+(v)| <= min
+        // exact |N+(u) n N+(v)| when known, else its bound min(du, dv)
+        int64_t b = esize ? int64_t(esize[e]) : (du < dv ? du : dv);
         keep[e] = e >= lo && e < hi && b >= min_d && (!vsel || vsel[u]);
         key[e] = uint32_t(b);  // bound on the task's locals: routes it to the warp/CTA kernel
     }
@@ -671,6 +694,29 @@ __global__ void k_split_point(const uint32_t *__restrict__ keys, int64_t n, uint
         else hi = mid;
     }
     *out = int32_t(lo);
+}
+
+// exact edge-task sizes |N+(u) n N+(v)| (bitgraph.py:67-86 locals count):
+// warp per edge, lanes over the shorter out-list, binary search in the longer
+__global__ void k_edge_sizes(const int64_t *__restrict__ orow, const int32_t *__restrict__ ocol,
+                             const int32_t *__restrict__ ocoo, int64_t m,
+                             int32_t *__restrict__ esize) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
+    const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t e = warp; e < m; e += nwarps) {
+        const int32_t u = ocoo[e], v = ocol[e];
+        int64_t ab = orow[u], ae = orow[u + 1], bb = orow[v], be = orow[v + 1];
+        if (ae - ab > be - bb) {
+            int64_t t0 = ab, t1 = ae;
+            ab = bb; ae = be; bb = t0; be = t1;
+        }
+        const int la = int(ae - ab), lb = int(be - bb);
+        int c = 0;
+        for (int i = lane; i < la; i += 32) c += gl_contains(ocol + bb, lb, ocol[ab + i]) ? 1 : 0;
+        for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+        if (lane == 0) esize[e] = c;
+    }
 }
 
 __global__ void k_mark_roots(const int32_t *__restrict__ roots, int64_t n,
@@ -738,7 +784,7 @@ int64_t build_tasks(kc_graph *g, int scheme, int64_t lo, int64_t hi, int min_d, 
             key.as<uint32_t>());
     } else {
         k_edge_select<<<grid_1d(N, g->num_sms), 256, 0, g->stream>>>(
-            g->orow_ptr, g->ocoo, g->ocol, N, lo, hi, min_d, vsel, keep.as<uint8_t>(),
+            g->orow_ptr, g->ocoo, g->ocol, N, lo, hi, min_d, vsel, g->esize, keep.as<uint8_t>(),
             key.as<uint32_t>());
     }
     k_iota<<<grid_1d(N, g->num_sms), 256, 0, g->stream>>>(ids.as<int32_t>(), N);
@@ -803,7 +849,7 @@ void launch_wpl(kc_graph *g, CountParams &p, int grid_override, Keep &keep,
     p.fw = MODE == MODE_PIVOT ? 64 * WPL + 4 : 32 * WPL + 4;
     const int need = frames_needed(MODE, p.t, p.dcap);
     auto area_words = [&](int nsm) {
-        size_t w = (MODE == MODE_PIVOT ? 64 * WPL : 0) +
+        size_t w = (MODE == MODE_PIVOT ? 64 * WPL + kStealCap * (32 * WPL + 4) : 0) +
                    size_t(NW) * (dpad + 32 * WPL + kct::kSmallWords + hist_words +
                                  size_t(nsm) * p.fw);
         if (p.scheme == KC_SCHEME_EDGE) w = std::max(w, dpad);
@@ -934,6 +980,12 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
     // edge scheme's sub-graph) and counts u's own visit, so counts and
     // visits are exactly the vertex scheme's (engine_orient.py:32-79).
     const bool split = !pivot && a->scheme == KC_SCHEME_VERTEX && t >= 4;
+    if ((split || a->scheme == KC_SCHEME_EDGE) && !g->esize && g->m_dir > 0) {
+        g->esize = kc_alloc<int32_t>(g->m_dir, g->stream);
+        k_edge_sizes<<<g->num_sms * 16, 256, 0, g->stream>>>(g->orow_ptr, g->ocol, g->ocoo,
+                                                             g->m_dir, g->esize);
+        KC_CUDA(cudaGetLastError());
+    }
     DevBuf tasks;
     int64_t n_big = 0;
     const int64_t n_tasks =
@@ -950,8 +1002,8 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
                               vsel.as<uint8_t>());
     }
 
-    DevBuf outs(8 * (16 + size_t(kSmidSlots)));
-    KC_CUDA(cudaMemsetAsync(outs.p, 0, 8 * (16 + size_t(kSmidSlots)), g->stream));
+    DevBuf outs(8 * (20 + size_t(kSmidSlots)));
+    KC_CUDA(cudaMemsetAsync(outs.p, 0, 8 * (20 + size_t(kSmidSlots)), g->stream));
     DevBuf dhist(pivot ? 8 * size_t(L * L) : 8);
     if (pivot) KC_CUDA(cudaMemsetAsync(dhist.p, 0, 8 * size_t(L * L), g->stream));
 
@@ -1000,27 +1052,31 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
     KC_CUDA(cudaEventRecord(e_fork, g->stream));
     KC_CUDA(cudaStreamWaitEvent(g->aux, e_fork, 0));
     if (split) {
-        if (n_items > 0) {
+        if (n_items_big > 0) {
+            CountParams b = p;
+            b.scheme = KC_SCHEME_EDGE;
+            b.t = t - 1;
+            b.split = 1;
+            b.tasks = items.as<int32_t>();
+            b.n_tasks = n_items_big;
+            b.task_counter = o + 8 + kSmidSlots + 5;
+            launch<MODE_ORIENT>(g, b, 0, keep, g->stream);
+        }
+        if (n_items - n_items_big > 0) {
             CountParams q = p;
             q.scheme = KC_SCHEME_EDGE;
             q.t = t - 1;
             q.split = 1;
-            q.tasks = items.as<int32_t>();
-            q.n_tasks = n_items;
+            q.tasks = items.as<int32_t>() + n_items_big;
+            q.n_tasks = n_items - n_items_big;
             q.task_counter = o + 8 + kSmidSlots + 2;
-            launch_warp<MODE_ORIENT>(g, q, keep, g->stream);
+            launch_warp<MODE_ORIENT>(g, q, keep, g->aux);
         }
         if (n_tasks - n_big > 0) {
             CountParams q = p;
             q.tasks = tasks.as<int32_t>() + n_big;
             q.n_tasks = n_tasks - n_big;
             launch_warp<MODE_ORIENT>(g, q, keep, g->aux);
-        }
-    } else if (a->scheme == KC_SCHEME_EDGE) {
-        if (n_tasks > 0) {
-            CountParams q = p;
-            if (pivot) launch_warp<MODE_PIVOT>(g, q, keep, g->stream);
-            else launch_warp<MODE_ORIENT>(g, q, keep, g->stream);
         }
     } else {
         if (n_big > 0) {

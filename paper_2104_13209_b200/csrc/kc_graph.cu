@@ -423,6 +423,8 @@ void kc_free_dag(kc_graph *g) {
     if (g->orow_ptr) kc_free(g->orow_ptr, g->stream);
     if (g->ocol) kc_free(g->ocol, g->stream);
     if (g->ocoo) kc_free(g->ocoo, g->stream);
+    if (g->esize) kc_free(g->esize, g->stream);
+    g->esize = nullptr;
     g->rank = nullptr;
     g->orow_ptr = nullptr;
     g->ocol = nullptr;

@@ -55,6 +55,7 @@ struct kc_graph {
     int64_t *orow_ptr = nullptr; // [n+1]
     int32_t *ocol = nullptr;     // [m]
     int32_t *ocoo = nullptr;     // [m]
+    int32_t *esize = nullptr;    // [m] |N+(u) n N+(v)| per oriented edge (lazy, edge tasks)
     // reusable scratch
     void *tmp = nullptr;
     size_t tmp_bytes = 0;

@@ -16,6 +16,10 @@
 // the j-th member) and word-sparse over C: only the nonzero words of C
 // (one ballot) are visited, each broadcast from its owner lane by __shfl_sync.
 //
+// Work accounting: `work` counts tree units (a visit, or one candidate
+// scored by a pivot choice); the kernels scale a task's units by its row
+// width ceil(d/32), which is SURVEY.md §8(d)'s algorithmic word count.
+//
 // Frames of the explicit DFS stack hold only the candidate set (and, for the
 // pivot engine, the branch set and two scalars); the "remaining" cursor set is
 // recomputed from the last expanded vertex, so a frame is 32*WPL (+32*WPL+4)
@@ -175,7 +179,7 @@ __device__ __forceinline__ int score_sum(const uint32_t *__restrict__ rows, int 
         const int v = ok ? list[i] : 0;
         acc += ull(cover<WPL>(rows, RS, C, v, ok));
     }
-    if (lane == 0) work += ull(n) * W;
+    if (lane == 0) work += ull(n);
     __syncwarp();
     return n;
 }
@@ -249,7 +253,7 @@ __device__ __forceinline__ void score_pairs(const uint32_t *__restrict__ rows, i
         }
         acc += a;
         visits += x_seen;
-        work += ull(W) * (1 + x_seen);
+        work += ull(1 + x_seen);
     }
     __syncwarp();
 }
@@ -274,7 +278,7 @@ __device__ __forceinline__ int select_pivot(const uint32_t *__restrict__ rows, i
         const ull y = __shfl_xor_sync(FULL, best, o);
         best = y > best ? y : best;
     }
-    if (lane == 0) work += ull(n) * W;
+    if (lane == 0) work += ull(n);
     __syncwarp();
     return int(0xffffffffu - uint32_t(best & 0xffffffffull));
 }
@@ -560,7 +564,7 @@ __device__ void orient_subtree(const uint32_t *__restrict__ rows, int RS, int W,
         }
         if (lane == 0) {
             ++visits;
-            work += W;
+            work += 1;
         }
         Set<WPL> X;
         const uint32_t *rv = rows + v * RS;
@@ -615,37 +619,69 @@ __device__ __forceinline__ bool pivot_try_small(const uint32_t *__restrict__ row
     return true;
 }
 
+// ---------------------------------------------------------------------------
+// CTA-local work sharing for the pivot walk of a big task.  A warp that has
+// run out of root branches parks as idle; a busy warp that creates an
+// L-tier child while some warp is idle hands the child (its set, depth and
+// pivot count -- everything the subtree needs) to a shared-memory stack
+// instead of descending into it.  All state changes happen under a spin lock
+// held by lane 0; termination = every warp idle and the stack empty.
+// ---------------------------------------------------------------------------
+struct StealStack {
+    uint32_t *items;  // cap x iw words: [C: 32*WPL][s][npv]
+    int *lock, *size, *idle;
+    int cap, iw, nwarps;
+    __device__ __forceinline__ void acquire() const {
+        while (atomicCAS(lock, 0, 1) != 0) __nanosleep(32);
+        __threadfence_block();
+    }
+    __device__ __forceinline__ void release() const {
+        __threadfence_block();
+        atomicExch(lock, 0);
+    }
+};
+
 template <int WPL>
-__device__ void pivot_subtree(const uint32_t *__restrict__ rows, int RS, int W, int t, bool allk,
-                              int v0, int piv0, const uint32_t *S0, const uint32_t *P0,
-                              const Frames &F, int *list, const SmallScratch &SS,
-                              const PivotLeafSink &sink, ull &visits, ull &work) {
-    const int lane = threadIdx.x & 31;
-    const int np0 = v0 == piv0 ? 1 : 0;
-    if (!allk && 1 - t > np0) return;  // engine_pivot.py:152-153
+__device__ __forceinline__ bool steal_push(const StealStack &q, const Set<WPL> &X, int s, int npv,
+                                           int lane) {
+    // heuristic pre-check without the lock
+    if (*(volatile int *)q.idle == 0 || *(volatile int *)q.size >= q.cap) return false;
+    int slot = -1;
     if (lane == 0) {
-        ++visits;
-        work += W;
+        q.acquire();
+        if (*(volatile int *)q.size < q.cap) slot = *(volatile int *)q.size;
+        else q.release();
     }
-    Set<WPL> C;
-    {
-        const uint32_t *rv = rows + v0 * RS;
-#pragma unroll
-        for (int p = 0; p < WPL; ++p) {
-            const int w = p * 32 + lane;
-            C.w[p] = w < W ? (S0[w] & rv[w] & ~(P0[w] & below_mask(w, v0))) : 0u;
-        }
+    slot = __shfl_sync(FULL, slot, 0);
+    if (slot < 0) return false;
+    uint32_t *it = q.items + slot * q.iw;
+    store_set<WPL>(it, X, lane);
+    if (lane == 0) {
+        it[32 * WPL] = uint32_t(s);
+        it[32 * WPL + 1] = uint32_t(npv);
     }
-    if (!any_set<WPL>(C)) {
-        if ((allk || 1 >= t) && lane == 0) sink.add(1, np0);
-        return;
+    __syncwarp();
+    if (lane == 0) {
+        __threadfence_block();
+        *(volatile int *)q.size = slot + 1;
+        q.release();
     }
-    if (!allk && 2 - t > np0 + 1) return;  // dead child
-    if (pivot_try_small<WPL>(rows, RS, W, C, 1, np0, t, allk, list, SS, sink, lane, visits, work))
+    __syncwarp();
+    return true;
+}
+
+// Walk the subtree of a fresh child set C (nonempty, not dead) at frame s0
+// with pivot count npv (engine_pivot.py:117-233 from that node down).
+template <int WPL>
+__device__ void pivot_from(const uint32_t *__restrict__ rows, int RS, int W, int t, bool allk,
+                           Set<WPL> C, const int s0, int npv, const Frames &F, int *list,
+                           const SmallScratch &SS, const PivotLeafSink &sink,
+                           const StealStack *q, ull &visits, ull &work) {
+    const int lane = threadIdx.x & 31;
+    if (pivot_try_small<WPL>(rows, RS, W, C, s0, npv, t, allk, list, SS, sink, lane, visits, work))
         return;
     const int PO = 32 * WPL, SC = 64 * WPL;  // P offset, scalars offset
-    int s = 1;
-    int npv = np0;
+    int s = s0;
     int piv = select_pivot<WPL>(rows, RS, C, list, lane, work, W);
     Set<WPL> P;
     {
@@ -654,9 +690,10 @@ __device__ void pivot_subtree(const uint32_t *__restrict__ rows, int RS, int W, 
         for (int p = 0; p < WPL; ++p) P.w[p] = C.w[p] & ~rp.w[p];
     }
     Set<WPL> R = P;
-    if (!allk && 2 - t > npv) restrict_to(R, piv, lane);
+    // engine_pivot.py:152-153: a frame with deficit npv+1 only branches on its pivot
+    if (!allk && s + 1 - t > npv) restrict_to(R, piv, lane);
     {
-        uint32_t *f = F.at(1);
+        uint32_t *f = F.at(s);
         store_set<WPL>(f, C, lane);
         store_set<WPL>(f + PO, P, lane);
         if (lane == 0) {
@@ -667,7 +704,8 @@ __device__ void pivot_subtree(const uint32_t *__restrict__ rows, int RS, int W, 
     for (;;) {
         const int v = next_bit<WPL>(R, lane);
         if (v < 0) {
-            if (--s == 0) break;
+            if (s == s0) break;
+            --s;
             const uint32_t *f = F.at(s);
             C = load_set<WPL>(f, lane);
             P = load_set<WPL>(f + PO, lane);
@@ -683,7 +721,7 @@ __device__ void pivot_subtree(const uint32_t *__restrict__ rows, int RS, int W, 
         if (!allk && s + 1 - t > np2) continue;
         if (lane == 0) {
             ++visits;
-            work += W;
+            work += 1;
         }
         Set<WPL> X;
         const uint32_t *rv = rows + v * RS;
@@ -694,7 +732,10 @@ __device__ void pivot_subtree(const uint32_t *__restrict__ rows, int RS, int W, 
             X.w[p] = w < W ? (C.w[p] & rv[w] & ~(P.w[p] & below_mask(w, v))) : 0u;
         }
         if (any_set<WPL>(X)) {
-            if (!allk && s + 2 - t > np2 + 1) continue;  // dead child (see pivot_small)
+            // a child whose every branch would be pruned adds neither visits nor leaves
+            if (!allk && s + 2 - t > np2 + 1) continue;
+            if (q && warp_count<WPL>(X) > 32 && steal_push<WPL>(*q, X, s + 1, np2, lane))
+                continue;
             if (pivot_try_small<WPL>(rows, RS, W, X, s + 1, np2, t, allk, list, SS, sink, lane,
                                      visits, work))
                 continue;
@@ -717,6 +758,88 @@ __device__ void pivot_subtree(const uint32_t *__restrict__ rows, int RS, int W, 
             }
         } else if (allk || s + 1 >= t) {
             if (lane == 0) sink.add(s + 1, np2);
+        }
+    }
+}
+
+// One root-level branch v0 of the task (frame 0 sets S0 / P0 in smem).
+template <int WPL>
+__device__ void pivot_subtree(const uint32_t *__restrict__ rows, int RS, int W, int t, bool allk,
+                              int v0, int piv0, const uint32_t *S0, const uint32_t *P0,
+                              const Frames &F, int *list, const SmallScratch &SS,
+                              const PivotLeafSink &sink, ull &visits, ull &work,
+                              const StealStack *q = nullptr) {
+    const int lane = threadIdx.x & 31;
+    const int np0 = v0 == piv0 ? 1 : 0;
+    if (!allk && 1 - t > np0) return;  // engine_pivot.py:152-153
+    if (lane == 0) {
+        ++visits;
+        work += 1;
+    }
+    Set<WPL> C;
+    {
+        const uint32_t *rv = rows + v0 * RS;
+#pragma unroll
+        for (int p = 0; p < WPL; ++p) {
+            const int w = p * 32 + lane;
+            C.w[p] = w < W ? (S0[w] & rv[w] & ~(P0[w] & below_mask(w, v0))) : 0u;
+        }
+    }
+    if (!any_set<WPL>(C)) {
+        if ((allk || 1 >= t) && lane == 0) sink.add(1, np0);
+        return;
+    }
+    if (!allk && 2 - t > np0 + 1) return;  // dead child
+    pivot_from<WPL>(rows, RS, W, t, allk, C, 1, np0, F, list, SS, sink, q, visits, work);
+}
+
+// Idle loop of the work-sharing protocol: pop and walk stolen subtrees until
+// every warp is idle and the stack is empty.
+template <int WPL>
+__device__ void pivot_steal_loop(const uint32_t *__restrict__ rows, int RS, int W, int t,
+                                 bool allk, const Frames &F, int *list, const SmallScratch &SS,
+                                 const PivotLeafSink &sink, const StealStack &q, ull &visits,
+                                 ull &work) {
+    const int lane = threadIdx.x & 31;
+    if (lane == 0) {
+        q.acquire();
+        ++*(volatile int *)q.idle;
+        q.release();
+    }
+    for (;;) {
+        int slot = -1, done = 0;
+        if (lane == 0) {
+            // poll without the lock; lock only to pop or to confirm termination
+            while (*(volatile int *)q.size == 0 && *(volatile int *)q.idle < q.nwarps)
+                __nanosleep(64);
+            q.acquire();
+            const int sz = *(volatile int *)q.size;
+            if (sz > 0) {
+                slot = sz - 1;  // popped under the lock; data read below, lock held
+                *(volatile int *)q.idle -= 1;
+            } else {
+                done = *(volatile int *)q.idle == q.nwarps;
+                q.release();
+            }
+        }
+        slot = __shfl_sync(FULL, slot, 0);
+        done = __shfl_sync(FULL, done, 0);
+        if (done) break;
+        if (slot < 0) continue;
+        const uint32_t *it = q.items + slot * q.iw;
+        const Set<WPL> X = load_set<WPL>(it, lane);
+        const int s = int(it[32 * WPL]);
+        const int npv = int(it[32 * WPL + 1]);
+        __syncwarp();
+        if (lane == 0) {
+            *(volatile int *)q.size = slot;
+            q.release();
+        }
+        pivot_from<WPL>(rows, RS, W, t, allk, X, s, npv, F, list, SS, sink, &q, visits, work);
+        if (lane == 0) {
+            q.acquire();
+            ++*(volatile int *)q.idle;
+            q.release();
         }
     }
 }
