@@ -3,11 +3,14 @@
 The counting kernel (k_count: fused sub-graph extraction + traversal) has two
 ceilings and reports against the one it is closer to:
 
-* ``alu``: traversal word-ops -- one u32 bitmap word ANDed with the candidate
-  set and POPC'd or stored, counted by the kernel itself (visits x row words,
-  plus |cand| x row words per pivot choice) -- against the measured full-chip
-  AND+POPC rate with one operand streamed from shared memory (kc_probe, the
-  kernel's own access pattern; the register-only rate is reported beside it);
+* ``alu``: SURVEY.md §8(d)'s algorithmic traversal work -- for every task,
+  (visits + candidates scored by pivot choices) x ceil(d_task/32) u32 words
+  ANDed and POPC'd -- counted by the kernel itself, against the measured
+  full-chip AND+POPC rate with one operand streamed from shared memory
+  (kc_probe, the kernel's own access pattern; the register-only rate is
+  reported beside it).  The kernel executes fewer word operations than this
+  (sets of <= 32 members are compressed to one word), so the fraction is of
+  the reference algorithm's work, as §8(d) defines it;
 * ``hbm``: global bytes the extraction reads (root out-list, every local's
   out-list, row pointers), counted by the kernel, against the measured HBM
   copy bandwidth in MEASURED_PEAKS.json (else the profiling guide's fallback).
