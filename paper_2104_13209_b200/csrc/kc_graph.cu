@@ -214,16 +214,15 @@ __global__ void k_peel_coop(const int64_t *__restrict__ row_ptr, const int32_t *
         tail = end;
         degen = level > degen ? level : degen;
         while (end > head) {
-            // mark step
-            begin_step();
-            for (int64_t i = head + gtid; i < end; i += gsz) round_of[order[i]] = round;
-            grid.sync();
-            ++p;
-            // relax step: warp per frontier vertex decrements live neighbours;
-            // one that crosses level+1 -> level joins the next round's frontier
+            // mark + relax step: warp per frontier vertex marks it removed and
+            // decrements its not-yet-removed neighbours; one that crosses
+            // level+1 -> level joins the next round's frontier.  Decrementing
+            // a vertex of the current frontier (not marked yet) is harmless:
+            // its degree is <= level, so it can never cross level+1 -> level.
             begin_step();
             for (int64_t i = head + gwarp; i < end; i += nwarps) {
                 const int32_t v = order[i];
+                if (lane == 0) round_of[v] = round;
                 for (int64_t e = row_ptr[v] + lane; e < row_ptr[v + 1]; e += 32) {
                     const int32_t w = col[e];
                     if (round_of[w] >= 0) continue;
@@ -441,19 +440,21 @@ static void degeneracy_rank(kc_graph *g, int64_t *degeneracy, int64_t *rounds_ou
     int32_t *round_of = kc_alloc<int32_t>(n, g->stream);
     int32_t *order = kc_alloc<int32_t>(n, g->stream);
     int32_t *ctl = kc_alloc<int32_t>(8, g->stream);
+    // one 1024-thread CTA per SM: grid barriers cost grow with the CTA count
+    constexpr int kPeelThreads = 1024;
     int per_sm = 0;
-    KC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_peel_coop, kThreads, 0));
+    KC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_peel_coop, kPeelThreads, 0));
     KC_REQUIRE(per_sm > 0, KC_ECUDA, "peel kernel cannot be resident");
-    int grid = per_sm * g->num_sms;
-    const int64_t want = (n + kThreads - 1) / kThreads;
+    int grid = g->num_sms;
+    const int64_t want = (n + kPeelThreads - 1) / kPeelThreads;
     if (want < grid) grid = int(want < 1 ? 1 : want);
     const int64_t *rp = g->row_ptr;
     const int32_t *cl = g->col;
     int64_t nn = n;
     void *args[] = {(void *)&rp, (void *)&cl, (void *)&nn, (void *)&deg, (void *)&round_of,
                     (void *)&order, (void *)&ctl};
-    KC_CUDA(cudaLaunchCooperativeKernel((void *)k_peel_coop, dim3(grid), dim3(kThreads), args, 0,
-                                        g->stream));
+    KC_CUDA(cudaLaunchCooperativeKernel((void *)k_peel_coop, dim3(grid), dim3(kPeelThreads), args,
+                                        0, g->stream));
     int32_t h[8] = {0};
     KC_CUDA(cudaMemcpyAsync(h, ctl, sizeof(h), cudaMemcpyDeviceToHost, g->stream));
     KC_CUDA(cudaStreamSynchronize(g->stream));

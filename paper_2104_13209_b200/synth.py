@@ -22,7 +22,10 @@ def normalize(pairs) -> np.ndarray:
     hi = np.maximum(u, v)[keep]
     if lo.size == 0:
         return np.empty((0, 2), dtype=np.int64)
-    key = np.unique((lo.astype(np.uint64) << np.uint64(32)) | hi.astype(np.uint64))
+    key = (lo.astype(np.uint64) << np.uint64(32)) | hi.astype(np.uint64)
+    key.sort()  # sort + adjacent dedup == np.unique, without its hash-table cost
+    if key.size > 1:
+        key = key[np.concatenate(([True], key[1:] != key[:-1]))]
     out = np.empty((key.size, 2), dtype=np.int64)
     out[:, 0] = (key >> np.uint64(32)).astype(np.int64)
     out[:, 1] = (key & np.uint64(0xFFFFFFFF)).astype(np.int64)
