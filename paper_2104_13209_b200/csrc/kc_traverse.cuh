@@ -337,9 +337,13 @@ __device__ __forceinline__ void pairs_small(const uint32_t *srow, uint32_t C, in
     }
 }
 
-// orientation walk of a compressed subtree; C is frame s (s <= last - 1)
+// orientation walk of a compressed subtree; C is frame s (s <= last - 1).
+// The scalar frame stack lives in registers: lane j holds frame s0+j (the
+// depth of a <= 32-member subtree is < 32), pushed with a predicated move and
+// popped with two shuffles -- no shared memory, no warp barrier.
 __device__ void orient_small(const uint32_t *srow, uint32_t C, int s, int last, uint32_t *sstk,
                              int lane, ull &acc, ull &visits, ull &work) {
+    (void)sstk;
     if (s == last - 1) {
         pairs_small(srow, C, lane, acc, visits, work);
         __syncwarp();
@@ -347,20 +351,19 @@ __device__ void orient_small(const uint32_t *srow, uint32_t C, int s, int last, 
     }
     const int s0 = s;
     uint32_t R = C;
+    uint32_t fC = 0, fR = 0;  // this lane's frame (depth s0 + lane)
+    unsigned uvis = 0;        // uniform visit count of the sequential levels
     for (;;) {
         if (R == 0) {
             if (s == s0) break;
             --s;
-            C = sstk[2 * (s - s0)];
-            R = sstk[2 * (s - s0) + 1];
+            C = __shfl_sync(FULL, fC, s - s0);
+            R = __shfl_sync(FULL, fR, s - s0);
             continue;
         }
         const int v = __ffs(R) - 1;
         R &= R - 1u;
-        if (lane == 0) {
-            ++visits;
-            ++work;
-        }
+        ++uvis;
         const uint32_t X = C & srow[v];
         if (!X) continue;
         if (s + 2 == last) {
@@ -368,14 +371,17 @@ __device__ void orient_small(const uint32_t *srow, uint32_t C, int s, int last, 
             __syncwarp();
             continue;
         }
-        if (lane == 0) {
-            sstk[2 * (s - s0)] = C;
-            sstk[2 * (s - s0) + 1] = R;
+        if (lane == s - s0) {
+            fC = C;
+            fR = R;
         }
-        __syncwarp();
         ++s;
         C = X;
         R = X;
+    }
+    if (lane == 0) {
+        visits += uvis;
+        work += uvis;
     }
 }
 
@@ -425,62 +431,64 @@ struct PivotLeafSink {
 };
 
 // pivot walk of a compressed subtree rooted at a fresh child set C (frame s,
-// pivot count npv); frames: 5 words (C, P, piv, npv, R) per level
+// pivot count npv).  Frame stack in registers (lane j = frame s0+j, see
+// orient_small); visit / work counters uniform, added by lane 0 at the end.
 template <typename Sink>
 __device__ void pivot_small(const uint32_t *srow, uint32_t myrow, uint32_t C, int s, int npv,
                             int t, bool allk, uint32_t *sstk, const Sink &sink, int lane,
                             ull &visits, ull &work) {
+    (void)sstk;
     const int s0 = s;
     int piv = select_small(C, myrow, lane);
     uint32_t P = C & ~srow[piv];
     // engine_pivot.py:152-153 prunes branch v iff s+1-t > npv + [v == piv]:
     // a frame with deficit npv+1 can only branch on its pivot (always in P)
     uint32_t R = (!allk && s + 1 - t > npv) ? (P & (1u << piv)) : P;
-    work += lane == 0 ? ull(__popc(C)) : 0ull;
+    unsigned uvis = 0, uwork = unsigned(__popc(C));
+    uint32_t fC = 0, fP = 0, fR = 0, fPN = 0;  // this lane's frame; fPN = piv | npv << 8
     for (;;) {
         if (R == 0) {
             if (s == s0) break;
             --s;
-            const uint32_t *f = sstk + 5 * (s - s0);
-            C = f[0];
-            P = f[1];
-            piv = int(f[2]);
-            npv = int(f[3]);
-            R = f[4];
+            const int j = s - s0;
+            C = __shfl_sync(FULL, fC, j);
+            P = __shfl_sync(FULL, fP, j);
+            R = __shfl_sync(FULL, fR, j);
+            const uint32_t pn = __shfl_sync(FULL, fPN, j);
+            piv = int(pn & 0xffu);
+            npv = int(pn >> 8);
             continue;
         }
         const int v = __ffs(R) - 1;
         R &= R - 1u;
         const int np2 = npv + (v == piv ? 1 : 0);
         if (!allk && s + 1 - t > np2) continue;
-        if (lane == 0) {
-            ++visits;
-            ++work;
-        }
+        ++uvis;
         const uint32_t X = C & srow[v] & ~(P & ((1u << v) - 1u));
         if (X) {
             // a child whose every branch would be pruned adds neither visits
             // nor leaves: do not build it
             if (!allk && s + 2 - t > np2 + 1) continue;
-            if (lane == 0) {
-                uint32_t *f = sstk + 5 * (s - s0);
-                f[0] = C;
-                f[1] = P;
-                f[2] = uint32_t(piv);
-                f[3] = uint32_t(npv);
-                f[4] = R;
+            if (lane == s - s0) {
+                fC = C;
+                fP = P;
+                fR = R;
+                fPN = uint32_t(piv) | (uint32_t(npv) << 8);
             }
-            __syncwarp();
             ++s;
             npv = np2;
             C = X;
             piv = select_small(C, myrow, lane);
             P = C & ~srow[piv];
             R = (!allk && s + 1 - t > npv) ? (P & (1u << piv)) : P;
-            if (lane == 0) work += ull(__popc(C));
+            uwork += unsigned(__popc(C));
         } else if (allk || s + 1 >= t) {
             if (lane == 0) sink.add(s + 1, np2);
         }
+    }
+    if (lane == 0) {
+        visits += uvis;
+        work += ull(uvis) + uwork;
     }
 }
 
