@@ -167,8 +167,8 @@ def count_kernel_launches(step):
         for ev in prof.events():
             if ev.device_type.name == "CUDA" and not ev.name.startswith("Memcpy") \
                     and not ev.name.startswith("Memset"):
-                nm = ev.name.split("(")[0].replace("(anonymous namespace)::", "")
-                nm = nm.replace("void ", "").split("<")[0][-60:]
+                nm = ev.name.replace("(anonymous namespace)::", "").replace("void ", "")
+                nm = nm.split("(")[0].split("<")[0][-60:]
                 names[nm] = names.get(nm, 0) + 1
         return sum(names.values()), names
     except Exception as exc:  # profiler unavailable: report unknown

@@ -52,10 +52,18 @@ def raw(rep):
 def hot_sass(rep, top):
     rows = list(csv.reader(io.StringIO(
         ncu(["-i", rep, "--page", "source", "--csv", "--print-source", "sass"]))))
-    if len(rows) < 3:
+    hdr, data, seen = None, [], 0
+    for r in rows:  # one section per kernel; keep the first
+        if r and r[0] == "Address":
+            seen += 1
+            if seen > 1:
+                break
+            hdr = r
+            continue
+        if hdr and len(r) == len(hdr):
+            data.append(dict(zip(hdr, r)))
+    if not data:
         return []
-    hdr = rows[1]
-    data = [dict(zip(hdr, r)) for r in rows[2:] if len(r) == len(hdr)]
     key = "Warp Stall Sampling (All Samples)"
     tot = sum(float(d[key] or 0) for d in data) or 1.0
     stalls = [h for h in hdr if h.startswith("stall_") and "Not Issued" not in h]
