@@ -47,6 +47,8 @@ struct CountParams {
     int split;         // tasks are out-edges of split vertex roots (see kc_do_count)
     int32_t *overflow;   // warp kernel: edge tasks with more than kWarpD locals
     ull *overflow_n;
+    kct::GQueue gq;      // pivot: GPU-wide subtree queue of the warp-tier kernel
+    int use_gq;
     int dcap;          // max locals per task
     int wcap;          // ceil(dcap / 32)
     int group_size;    // reserved (sub-warp group size; traversal is warp-granular)
@@ -382,10 +384,19 @@ __global__ void __launch_bounds__(BLOCK) k_count(CountParams p) {
     F.fw = p.fw;
     F.gm = p.frames_global ? p.frames_global + (int64_t(blockIdx.x) * NW + warp) * p.frames_slot
                            : nullptr;
+    __shared__ int s_hc[2 * NW];
     kct::PivotLeafSink sink;
     sink.whist = whist;
     sink.g_hist = p.hist;
     sink.L = p.hist_dim;
+    sink.gq = (MODE == MODE_PIVOT && p.use_gq) ? &p.gq : nullptr;
+    sink.l2g = l2g;
+    sink.hc = s_hc + 2 * warp;
+    if ((tid & 31) == 0) {
+        sink.hc[0] = 0;
+        sink.hc[1] = 0;
+        if (sink.gq) atomicAdd(p.gq.ctl + 3, 1);  // busy: this warp may push to the warp tier
+    }
 
     for (int i = tid & 31; i < hist_cells; i += 32) whist[i] = 0;
     ull acc = 0, visits = 0, tasks = 0, work = 0, bytes = 0;
@@ -447,6 +458,11 @@ __global__ void __launch_bounds__(BLOCK) k_count(CountParams p) {
     }
     __syncthreads();
     if (MODE == MODE_PIVOT) sink.flush(tid & 31);
+    if (sink.gq && (tid & 31) == 0) {
+        p.gq.acquire();
+        p.gq.set(3, p.gq.vol(3) - 1);
+        p.gq.release();
+    }
     if (MODE != MODE_EXTRACT) flush_block<BLOCK>(p, acc, visits, tasks, work, bytes, s_red);
 }
 
@@ -457,6 +473,7 @@ __global__ void __launch_bounds__(BLOCK) k_count(CountParams p) {
 // in the S-tier (their rows already are one word).
 // ---------------------------------------------------------------------------
 constexpr int kWarpD = 128;
+constexpr int kGqCap = 4096;  // GPU-wide subtree queue slots (pivot)
 constexpr int kSplitD = 32;  // orientation/vertex: roots above this are split into edge items
 
 __device__ __forceinline__ bool gl_contains(const int32_t *__restrict__ a, int n, int32_t x) {
@@ -467,6 +484,32 @@ __device__ __forceinline__ bool gl_contains(const int32_t *__restrict__ a, int n
         else hi = mid;
     }
     return lo < n && __ldg(a + lo) == x;
+}
+
+// warp-level bit matrix of the sub-graph induced by the sorted vertices l2g[0..d)
+// (bitgraph.py:89-111: bit j of row i <=> arc l2g[i] -> l2g[j], or either arc)
+__device__ void warp_rows(const CountParams &p, const int32_t *l2g, int d, uint32_t *rows,
+                          bool directed, ull &bytes) {
+    const int lane = threadIdx.x & 31;
+    const int W = (d + 31) >> 5, RS = row_stride(W);
+    for (int i = lane; i < d * RS; i += 32) rows[i] = 0u;
+    __syncwarp();
+    const int32_t lo_id = l2g[0], hi_id = l2g[d - 1];
+    for (int i = 0; i < d; ++i) {
+        const int32_t gi = l2g[i];
+        const int64_t beg = p.orow[gi], end = p.orow[gi + 1];
+        if (lane == 0) bytes += 16 + 4ull * (end - beg);
+        for (int64_t e = beg + lane; e < end; e += 32) {
+            const int32_t x = p.ocol[e];
+            if (x < lo_id || x > hi_id) continue;
+            const int j = smem_find(l2g, d, x);
+            if (j >= 0) {
+                atomicOr(&rows[i * RS + (j >> 5)], 1u << (j & 31));
+                if (!directed) atomicOr(&rows[j * RS + (i >> 5)], 1u << (i & 31));
+            }
+        }
+    }
+    __syncwarp();
 }
 
 // warp-level K4: locals + bit matrix of one task (d <= kWarpD)
@@ -502,25 +545,7 @@ __device__ int warp_build(const CountParams &p, int32_t task, int32_t *l2g, uint
     __syncwarp();
     if (d > kWarpD) return d;  // caller defers the task to the CTA kernel
     if (!need_rows || d == 0) return d;
-    const int W = (d + 31) >> 5, RS = row_stride(W);
-    for (int i = lane; i < d * RS; i += 32) rows[i] = 0u;
-    __syncwarp();
-    const int32_t lo_id = l2g[0], hi_id = l2g[d - 1];
-    for (int i = 0; i < d; ++i) {
-        const int32_t gi = l2g[i];
-        const int64_t beg = p.orow[gi], end = p.orow[gi + 1];
-        if (lane == 0) bytes += 16 + 4ull * (end - beg);
-        for (int64_t e = beg + lane; e < end; e += 32) {
-            const int32_t x = p.ocol[e];
-            if (x < lo_id || x > hi_id) continue;
-            const int j = smem_find(l2g, d, x);
-            if (j >= 0) {
-                atomicOr(&rows[i * RS + (j >> 5)], 1u << (j & 31));
-                if (!directed) atomicOr(&rows[j * RS + (i >> 5)], 1u << (i & 31));
-            }
-        }
-    }
-    __syncwarp();
+    warp_rows(p, l2g, d, rows, directed, bytes);
     return d;
 }
 
@@ -553,11 +578,20 @@ __global__ void __launch_bounds__(BLOCK) k_count_warp(CountParams p) {
     F.fw = p.fw;
     F.gm = p.frames_global ? p.frames_global + (int64_t(blockIdx.x) * NW + warp) * p.frames_slot
                            : nullptr;
+    __shared__ int s_hc[2 * NW];
     kct::PivotLeafSink sink;
     sink.whist = whist;
     sink.g_hist = p.hist;
     sink.L = p.hist_dim;
+    sink.gq = (MODE == MODE_PIVOT && p.use_gq) ? &p.gq : nullptr;
+    sink.l2g = l2g;
+    sink.hc = s_hc + 2 * warp;
     for (int i = lane; i < hist_cells; i += 32) whist[i] = 0;
+    if (lane == 0) {
+        sink.hc[0] = 0;
+        sink.hc[1] = 0;
+        if (sink.gq) atomicAdd(p.gq.ctl + 3, 1);  // busy: this warp may push
+    }
     __syncwarp();
 
     ull acc = 0, visits = 0, tasks = 0, work = 0, bytes = 0;
@@ -640,6 +674,80 @@ __global__ void __launch_bounds__(BLOCK) k_count_warp(CountParams p) {
         }
         work = wt0 + (work - wt0) * ull(W);
         __syncwarp();
+    }
+    if (MODE == MODE_PIVOT && sink.gq) {
+        // task queue drained: serve subtrees handed over by busy warps
+        const kct::GQueue &q = p.gq;
+        if (lane == 0) {
+            q.acquire();
+            q.set(3, q.vol(3) - 1);
+            q.set(2, q.vol(2) + 1);
+            q.release();
+        }
+        for (;;) {
+            int slot = -1, done = 0;
+            if (lane == 0) {
+                // wait while someone may still push; give the SM back after
+                // ~1 ms without items (a pusher re-checks `hungry` under the
+                // lock, so leaving never strands an item)
+                int spins = 0;
+                while (q.vol(1) == 0 && q.vol(3) > 0 && spins < 4000) {
+                    __nanosleep(256);
+                    ++spins;
+                }
+                q.acquire();
+                const int sz = q.vol(1);
+                if (sz > 0) {
+                    slot = sz - 1;  // lock kept while the item is copied out
+                    q.set(2, q.vol(2) - 1);
+                    q.set(3, q.vol(3) + 1);
+                } else {
+                    if (q.vol(3) == 0 || spins >= 4000) {
+                        done = 1;
+                        q.set(2, q.vol(2) - 1);
+                    }
+                    q.release();
+                }
+            }
+            slot = __shfl_sync(kct::FULL, slot, 0);
+            done = __shfl_sync(kct::FULL, done, 0);
+            if (done) break;
+            if (slot < 0) continue;
+            const uint32_t *it = q.items + int64_t(slot) * kct::kGItemWords;
+            const int n = int(it[0]), s0 = int(it[1]), npv = int(it[2]);
+            for (int i = lane; i < n; i += 32) l2g[i] = int32_t(it[4 + i]);
+            __syncwarp();
+            if (lane == 0) {
+                q.set(1, slot);
+                q.release();
+            }
+            // the subtree of X depends only on the sub-graph induced by X
+            warp_rows(p, l2g, n, rows, false, bytes);
+            const int W = (n + 31) >> 5, RS = row_stride(W);
+            const ull wt0 = work;
+            if (W == 1) {
+                const uint32_t all = n >= 32 ? kct::FULL : ((1u << n) - 1u);
+                const uint32_t myrow = lane < n ? rows[lane] : 0u;
+                kct::pivot_small(rows, myrow, all, s0, npv, t, allk, SS.sstk, sink, lane, visits,
+                                 work);
+            } else {
+                kct::Set<WPL> A;
+                {
+                    const int lo = lane << 5;
+                    A.w[0] = lo >= n ? 0u : (lo + 32 <= n ? kct::FULL : ((1u << (n - lo)) - 1u));
+                }
+                kct::pivot_from<WPL>(rows, RS, W, t, allk, A, s0, npv, F, list, SS, sink, nullptr,
+                                     visits, work);
+            }
+            work = wt0 + (work - wt0) * ull(W);
+            if (lane == 0) {
+                q.acquire();
+                q.set(3, q.vol(3) - 1);
+                q.set(2, q.vol(2) + 1);
+                q.release();
+            }
+            __syncwarp();
+        }
     }
     if (MODE == MODE_PIVOT) sink.flush(lane);
     __syncthreads();
@@ -1038,6 +1146,12 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
     KC_CUDA(cudaEventCreateWithFlags(&e_fork, cudaEventDisableTiming));
     KC_CUDA(cudaEventCreateWithFlags(&e_join, cudaEventDisableTiming));
     KC_CUDA(cudaEventRecord(e0, g->stream));
+    DevBuf gq_items(pivot ? 4 * size_t(kGqCap) * kct::kGItemWords : 4), gq_ctl(16);
+    KC_CUDA(cudaMemsetAsync(gq_ctl.p, 0, 16, g->stream));
+    p.gq.items = gq_items.as<uint32_t>();
+    p.gq.ctl = gq_ctl.as<int>();
+    p.gq.cap = kGqCap;
+    p.use_gq = pivot ? 1 : 0;
     Keep keep;
     // Edge tasks (and split items) all go to the warp-per-task kernel; the few
     // whose intersection exceeds kWarpD locals are appended to an overflow

@@ -398,10 +398,94 @@ __device__ __forceinline__ int select_small(uint32_t C, uint32_t myrow, int lane
 // flushed to the global u64 L x L histogram at 2^31 and at kernel end.
 constexpr int kLeafHL = 32;
 constexpr int kLeafCells = kLeafHL * (kLeafHL + 1) / 2;
+
+// ---------------------------------------------------------------------------
+// GPU-wide subtree queue (pivot engine).  A busy warp that creates a child
+// set X of kPushMin..kGItemMax members while some warp of the warp-tier
+// kernel is hungry hands X over as an explicit, self-contained item: the
+// sorted GLOBAL vertex ids of X plus (depth, pivot count).  The thief builds
+// the sub-graph induced by exactly those vertices (ascending compact id, so
+// the relabelling preserves the reference's order and tie-breaks) and walks
+// X's subtree -- no dependence on the donor's task or bitmap.  Protocol
+// (all under one global spin lock, low traffic): `busy` counts warps that
+// may still push, `hungry` counts warps waiting for items; a hungry warp
+// exits only when busy == 0 and the stack is empty.
+// ---------------------------------------------------------------------------
+constexpr int kGItemMax = 128;
+constexpr int kGItemWords = 4 + kGItemMax;  // [n][s][npv][-][ids]
+constexpr int kPushMin = 6;
+struct GQueue {
+    uint32_t *items;  // cap x kGItemWords
+    int *ctl;         // [0] lock [1] size [2] hungry [3] busy
+    int cap;
+    __device__ __forceinline__ void acquire() const {
+        while (atomicCAS(ctl, 0, 1) != 0) __nanosleep(64);
+        __threadfence();
+    }
+    __device__ __forceinline__ void release() const {
+        __threadfence();
+        atomicExch(ctl, 0);
+    }
+    __device__ __forceinline__ int vol(int i) const { return *(volatile int *)(ctl + i); }
+    __device__ __forceinline__ void set(int i, int v) const { *(volatile int *)(ctl + i) = v; }
+};
+
 struct PivotLeafSink {
     uint32_t *whist;  // this warp's kLeafCells counters
     ull *g_hist;      // global L x L histogram
     int L;
+    // GPU-wide work sharing (nullptr: off)
+    const GQueue *gq;
+    const int32_t *l2g;  // local id -> global vertex id of the current universe
+    int *hc;             // per-warp smem: [0] countdown [1] cached hungry
+    // uniform: should a child of n members be handed to a hungry warp?
+    __device__ __forceinline__ bool want_push(int n, int lane) const {
+        if (!gq || n < kPushMin || n > kGItemMax) return false;
+        if (lane == 0 && --hc[0] <= 0) {
+            hc[0] = 32;
+            hc[1] = gq->vol(2);
+        }
+        __syncwarp();
+        return hc[1] > 0;
+    }
+    // reserve a slot (lock held by lane 0 on success); -1 when full / nobody hungry
+    __device__ __forceinline__ int reserve(int lane) const {
+        int slot = -1;
+        if (lane == 0) {
+            gq->acquire();
+            if (gq->vol(1) < gq->cap && gq->vol(2) > 0) slot = gq->vol(1);
+            else gq->release();
+        }
+        return __shfl_sync(0xffffffffu, slot, 0);
+    }
+    __device__ __forceinline__ void publish(int slot, int n, int s, int npv, int lane) const {
+        uint32_t *it = gq->items + int64_t(slot) * kGItemWords;
+        if (lane == 0) {
+            it[0] = uint32_t(n);
+            it[1] = uint32_t(s);
+            it[2] = uint32_t(npv);
+        }
+        __syncwarp();
+        if (lane == 0) {
+            __threadfence();
+            gq->set(1, slot + 1);
+            gq->release();
+        }
+        __syncwarp();
+    }
+    // S-tier child X (compressed ids; map = compressed -> local, nullptr = identity)
+    __device__ __forceinline__ bool push_small(uint32_t X, const int *map, int s, int npv,
+                                               int lane) const {
+        const int slot = reserve(lane);
+        if (slot < 0) return false;
+        uint32_t *ids = gq->items + int64_t(slot) * kGItemWords + 4;
+        if ((X >> lane) & 1u) {
+            const int local = map ? map[lane] : lane;
+            ids[__popc(X & ((1u << lane) - 1u))] = uint32_t(l2g[local]);
+        }
+        publish(slot, __popc(X), s, npv, lane);
+        return true;
+    }
     __device__ __forceinline__ void add(int len, int np) const {
         if (len < kLeafHL) {
             uint32_t &c = whist[len * (len + 1) / 2 + np];
@@ -436,7 +520,7 @@ struct PivotLeafSink {
 template <typename Sink>
 __device__ void pivot_small(const uint32_t *srow, uint32_t myrow, uint32_t C, int s, int npv,
                             int t, bool allk, uint32_t *sstk, const Sink &sink, int lane,
-                            ull &visits, ull &work) {
+                            ull &visits, ull &work, const int *map = nullptr) {
     (void)sstk;
     const int s0 = s;
     int piv = select_small(C, myrow, lane);
@@ -469,6 +553,9 @@ __device__ void pivot_small(const uint32_t *srow, uint32_t myrow, uint32_t C, in
             // a child whose every branch would be pruned adds neither visits
             // nor leaves: do not build it
             if (!allk && s + 2 - t > np2 + 1) continue;
+            // hand the child to a hungry warp (GPU-wide work sharing)
+            if (sink.want_push(__popc(X), lane) && sink.push_small(X, map, s + 1, np2, lane))
+                continue;
             if (lane == s - s0) {
                 fC = C;
                 fP = P;
@@ -623,7 +710,7 @@ __device__ __forceinline__ bool pivot_try_small(const uint32_t *__restrict__ row
     uint32_t myrow;
     const int n = compress<WPL>(rows, RS, X, list, S.srow, lane, myrow);
     pivot_small(S.srow, myrow, n == 32 ? FULL : ((1u << n) - 1u), s, npv, t, allk, S.sstk, sink,
-                lane, visits, work);
+                lane, visits, work, list);
     return true;
 }
 
@@ -675,6 +762,19 @@ __device__ __forceinline__ bool steal_push(const StealStack &q, const Set<WPL> &
         q.release();
     }
     __syncwarp();
+    return true;
+}
+
+// hand an L-tier child X (local ids of the current universe) to the queue
+template <int WPL>
+__device__ __forceinline__ bool push_large(const PivotLeafSink &sink, const Set<WPL> &X, int *list,
+                                           int s, int npv, int lane) {
+    const int slot = sink.reserve(lane);
+    if (slot < 0) return false;
+    const int n = compact<WPL>(X, list, lane);
+    uint32_t *ids = sink.gq->items + int64_t(slot) * kGItemWords + 4;
+    for (int i = lane; i < n; i += 32) ids[i] = uint32_t(sink.l2g[list[i]]);
+    sink.publish(slot, n, s, npv, lane);
     return true;
 }
 
@@ -742,8 +842,13 @@ __device__ void pivot_from(const uint32_t *__restrict__ rows, int RS, int W, int
         if (any_set<WPL>(X)) {
             // a child whose every branch would be pruned adds neither visits nor leaves
             if (!allk && s + 2 - t > np2 + 1) continue;
-            if (q && warp_count<WPL>(X) > 32 && steal_push<WPL>(*q, X, s + 1, np2, lane))
-                continue;
+            {
+                const int nx = warp_count<WPL>(X);
+                if (WPL == 1 && sink.want_push(nx, lane) &&
+                    push_large<WPL>(sink, X, list, s + 1, np2, lane))
+                    continue;
+                if (q && nx > 32 && steal_push<WPL>(*q, X, s + 1, np2, lane)) continue;
+            }
             if (pivot_try_small<WPL>(rows, RS, W, X, s + 1, np2, t, allk, list, SS, sink, lane,
                                      visits, work))
                 continue;
