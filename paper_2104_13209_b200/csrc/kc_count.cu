@@ -460,7 +460,7 @@ __global__ void __launch_bounds__(BLOCK) k_count(CountParams p) {
     if (MODE == MODE_PIVOT) sink.flush(tid & 31);
     if (sink.gq && (tid & 31) == 0) {
         p.gq.acquire();
-        p.gq.set(3, p.gq.vol(3) - 1);
+        atomicSub(p.gq.ctl + 3, 1);
         p.gq.release();
     }
     if (MODE != MODE_EXTRACT) flush_block<BLOCK>(p, acc, visits, tasks, work, bytes, s_red);
@@ -680,42 +680,50 @@ __global__ void __launch_bounds__(BLOCK) k_count_warp(CountParams p) {
         const kct::GQueue &q = p.gq;
         if (lane == 0) {
             q.acquire();
-            q.set(3, q.vol(3) - 1);
-            q.set(2, q.vol(2) + 1);
+            atomicSub(q.ctl + 3, 1);
+            atomicAdd(q.ctl + 2, 1);
             q.release();
         }
         for (;;) {
             int slot = -1, done = 0;
             if (lane == 0) {
-                // wait while someone may still push; give the SM back after
-                // ~1 ms without items (a pusher re-checks `hungry` under the
-                // lock, so leaving never strands an item)
-                int spins = 0;
-                while (q.vol(1) == 0 && q.vol(3) > 0 && spins < 4000) {
-                    __nanosleep(256);
-                    ++spins;
-                }
-                q.acquire();
-                const int sz = q.vol(1);
-                if (sz > 0) {
-                    slot = sz - 1;  // lock kept while the item is copied out
-                    q.set(2, q.vol(2) - 1);
-                    q.set(3, q.vol(3) + 1);
-                } else {
-                    if (q.vol(3) == 0 || spins >= 4000) {
-                        done = 1;
-                        q.set(2, q.vol(2) - 1);
+                // Poll without the lock; take it with a single try (no
+                // spinning on it: a pusher must never queue behind hundreds
+                // of hungry warps).  Give the SM back after ~1 ms without
+                // items -- a pusher re-checks `hungry` under the lock, so
+                // leaving never strands an item.
+                const unsigned jitter = (blockIdx.x * 7 + warp * 13) & 127;
+                for (int spins = 0;; ++spins) {
+                    const int sz = q.vol(1);
+                    const bool give_up = sz == 0 && (q.vol(3) == 0 || spins >= 4000);
+                    if ((sz > 0 || give_up) && atomicCAS(q.ctl, 0, 1) == 0) {
+                        __threadfence();
+                        const int sz2 = q.vol(1);
+                        if (sz2 > 0) {
+                            slot = sz2 - 1;  // lock kept while the item is copied out
+                            atomicSub(q.ctl + 2, 1);
+                            atomicAdd(q.ctl + 3, 1);
+                            break;
+                        }
+                        if (q.vol(3) == 0 || spins >= 4000) {
+                            done = 1;
+                            atomicSub(q.ctl + 2, 1);
+                            q.release();
+                            break;
+                        }
+                        q.release();
                     }
-                    q.release();
+                    __nanosleep(128 + jitter);
                 }
             }
             slot = __shfl_sync(kct::FULL, slot, 0);
             done = __shfl_sync(kct::FULL, done, 0);
             if (done) break;
-            if (slot < 0) continue;
+            // L2-coherent loads (__ldcg): this SM's L1 may hold an older item
+            // of the same slot
             const uint32_t *it = q.items + int64_t(slot) * kct::kGItemWords;
-            const int n = int(it[0]), s0 = int(it[1]), npv = int(it[2]);
-            for (int i = lane; i < n; i += 32) l2g[i] = int32_t(it[4 + i]);
+            const int n = int(__ldcg(it)), s0 = int(__ldcg(it + 1)), npv = int(__ldcg(it + 2));
+            for (int i = lane; i < n; i += 32) l2g[i] = int32_t(__ldcg(it + 4 + i));
             __syncwarp();
             if (lane == 0) {
                 q.set(1, slot);
@@ -742,8 +750,8 @@ __global__ void __launch_bounds__(BLOCK) k_count_warp(CountParams p) {
             work = wt0 + (work - wt0) * ull(W);
             if (lane == 0) {
                 q.acquire();
-                q.set(3, q.vol(3) - 1);
-                q.set(2, q.vol(2) + 1);
+                atomicSub(q.ctl + 3, 1);
+                atomicAdd(q.ctl + 2, 1);
                 q.release();
             }
             __syncwarp();

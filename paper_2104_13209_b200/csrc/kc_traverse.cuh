@@ -407,13 +407,16 @@ constexpr int kLeafCells = kLeafHL * (kLeafHL + 1) / 2;
 // the sub-graph induced by exactly those vertices (ascending compact id, so
 // the relabelling preserves the reference's order and tie-breaks) and walks
 // X's subtree -- no dependence on the donor's task or bitmap.  Protocol
-// (all under one global spin lock, low traffic): `busy` counts warps that
+// (stack slots under one global spin lock, low traffic; the `busy` and
+// `hungry` counters only ever change by atomics): `busy` counts warps that
 // may still push, `hungry` counts warps waiting for items; a hungry warp
-// exits only when busy == 0 and the stack is empty.
+// leaves only under the lock with the stack empty, so a pusher -- which
+// re-checks `hungry` under the lock -- can never strand an item.
 // ---------------------------------------------------------------------------
 constexpr int kGItemMax = 128;
 constexpr int kGItemWords = 4 + kGItemMax;  // [n][s][npv][-][ids]
-constexpr int kPushMin = 6;
+constexpr int kPushMin = 12;      // smaller children are cheaper to walk than to rebuild
+constexpr int kPushCooldown = 256;  // child decisions between two hand-overs of one warp
 struct GQueue {
     uint32_t *items;  // cap x kGItemWords
     int *ctl;         // [0] lock [1] size [2] hungry [3] busy
@@ -439,21 +442,28 @@ struct PivotLeafSink {
     const int32_t *l2g;  // local id -> global vertex id of the current universe
     int *hc;             // per-warp smem: [0] countdown [1] cached hungry
     // uniform: should a child of n members be handed to a hungry warp?
+    // Rate-limited: at most one hand-over per kPushCooldown decisions, so a
+    // donor keeps doing its own work and thieves get substantial subtrees.
     __device__ __forceinline__ bool want_push(int n, int lane) const {
         if (!gq || n < kPushMin || n > kGItemMax) return false;
         if (lane == 0 && --hc[0] <= 0) {
-            hc[0] = 32;
+            hc[0] = kPushCooldown;
             hc[1] = gq->vol(2);
         }
         __syncwarp();
-        return hc[1] > 0;
+        const bool w = hc[1] > 0;
+        __syncwarp();
+        if (w && lane == 0) hc[1] = 0;  // one hand-over per cooldown window
+        return w;
     }
     // reserve a slot (lock held by lane 0 on success); -1 when full / nobody hungry
     __device__ __forceinline__ int reserve(int lane) const {
         int slot = -1;
         if (lane == 0) {
             gq->acquire();
-            if (gq->vol(1) < gq->cap && gq->vol(2) > 0) slot = gq->vol(1);
+            // only while more warps are hungry than items are waiting
+            const int sz = gq->vol(1);
+            if (sz < gq->cap && sz < gq->vol(2)) slot = sz;
             else gq->release();
         }
         return __shfl_sync(0xffffffffu, slot, 0);
