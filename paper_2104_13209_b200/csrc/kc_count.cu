@@ -25,6 +25,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 #include <memory>
 #include <vector>
 
@@ -1159,7 +1160,14 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
     p.gq.items = gq_items.as<uint32_t>();
     p.gq.ctl = gq_ctl.as<int>();
     p.gq.cap = kGqCap;
-    p.use_gq = pivot ? 1 : 0;
+    // experimental (round 1): GPU-wide subtree hand-over, opt-in via KC_GQ=1 --
+    // it is exact but does not yet move the L-tier giant subtrees and its
+    // polling costs more than it saves on RMAT
+    static const bool gq_on = [] {
+        const char *e = getenv("KC_GQ");
+        return e && e[0] == '1';
+    }();
+    p.use_gq = pivot && gq_on ? 1 : 0;
     Keep keep;
     // Edge tasks (and split items) all go to the warp-per-task kernel; the few
     // whose intersection exceeds kWarpD locals are appended to an overflow

@@ -524,6 +524,44 @@ struct PivotLeafSink {
     }
 };
 
+// Take the lowest pending branch v of the shallowest stored frame (lane j
+// holds frame s0+j; `depth` frames are stored) and hand its child to the
+// queue.  A pruned / leaf / dead branch is consumed inline instead (it is
+// ordinary work: a visit and maybe a leaf); when the queue refuses the item
+// the branch is put back.  Ascending order within the frame is kept, so the
+// reference's "pruned bits below v" rule (engine_pivot.py:158-166) holds.
+template <typename Sink>
+__device__ __forceinline__ void donate_bottom(const uint32_t *srow, const int *map, int depth,
+                                              int s0, int t, bool allk, uint32_t fC, uint32_t fP,
+                                              uint32_t &fR, uint32_t fPN, const Sink &sink,
+                                              int lane, unsigned &uvis) {
+    const unsigned has = __ballot_sync(FULL, lane < depth && fR != 0);
+    if (!has) return;
+    const int j = __ffs(has) - 1;
+    const uint32_t jC = __shfl_sync(FULL, fC, j), jP = __shfl_sync(FULL, fP, j);
+    const uint32_t jR = __shfl_sync(FULL, fR, j), pn = __shfl_sync(FULL, fPN, j);
+    const int v = __ffs(jR) - 1;
+    if (lane == j) fR = jR & (jR - 1u);
+    const int sj = s0 + j, jpiv = int(pn & 0xffu), jnpv = int(pn >> 8);
+    const int np2 = jnpv + (v == jpiv ? 1 : 0);
+    if (!allk && sj + 1 - t > np2) return;  // pruned: not a visit
+    const uint32_t X = jC & srow[v] & ~(jP & ((1u << v) - 1u));
+    if (!X) {
+        ++uvis;
+        if ((allk || sj + 1 >= t) && lane == 0) sink.add(sj + 1, np2);
+        return;
+    }
+    if (!allk && sj + 2 - t > np2 + 1) {  // dead child
+        ++uvis;
+        return;
+    }
+    if (__popc(X) >= kPushMin && sink.push_small(X, map, sj + 1, np2, lane)) {
+        ++uvis;
+        return;
+    }
+    if (lane == j) fR = jR;  // refused: the branch stays with this warp
+}
+
 // pivot walk of a compressed subtree rooted at a fresh child set C (frame s,
 // pivot count npv).  Frame stack in registers (lane j = frame s0+j, see
 // orient_small); visit / work counters uniform, added by lane 0 at the end.
@@ -563,9 +601,11 @@ __device__ void pivot_small(const uint32_t *srow, uint32_t myrow, uint32_t C, in
             // a child whose every branch would be pruned adds neither visits
             // nor leaves: do not build it
             if (!allk && s + 2 - t > np2 + 1) continue;
-            // hand the child to a hungry warp (GPU-wide work sharing)
-            if (sink.want_push(__popc(X), lane) && sink.push_small(X, map, s + 1, np2, lane))
-                continue;
+            // GPU-wide work sharing: while some warp is hungry, donate the
+            // SHALLOWEST pending branch (the biggest subtree this warp still
+            // owns), classic work stealing from the bottom of the stack
+            if (sink.gq && s > s0 && sink.want_push(kPushMin, lane))
+                donate_bottom(srow, map, s - s0, s0, t, allk, fC, fP, fR, fPN, sink, lane, uvis);
             if (lane == s - s0) {
                 fC = C;
                 fP = P;
