@@ -54,6 +54,8 @@ def parse():
                     help="target CPU seconds of the oracle baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-configs", action="store_true",
+                    help="skip the side measurements of the other BASELINE.json configs")
     ap.add_argument("--per-k", default="4,7",
                     help="also time these k (1 warm-up + 2 timed steps each) into per_k")
     a = ap.parse_args()
@@ -316,6 +318,11 @@ def run_ours(a):
                           "ms_per_step": t2 / n_t, "cliques_per_s": r2.count * n_t / (t2 / 1e3),
                           "visits": r2.load.total, "steps": n_t, "warmup": warm}
 
+    # the other BASELINE.json configs (1 GPU only; 1 warm-up + 2 timed steps)
+    side = {}
+    if world == 1 and not a.no_configs:
+        side = other_configs(kc, time_steps, local)
+
     roof = roofline(kc, g, cfg, rep, a, local) if rank == 0 else None
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
@@ -333,12 +340,60 @@ def run_ours(a):
             "clocks": clk.summary(), "e2e": e2e, "gpu_launches": (n_launch * a.steps
                                                                   if n_launch else None),
             "gpu_launches_per_step": n_launch, "kernels": launch_names,
-            "roofline": roof, "cpu_baseline": cpu, "per_k": per_k,
+            "roofline": roof, "cpu_baseline": cpu, "per_k": per_k, "configs": side,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def other_configs(kc, time_steps, local):
+    """Side measurements of BASELINE.json configs 0, 2 and 3 (config 1 is the
+    headline; config 4 is the multi-GPU run of this script with --gpus N)."""
+    import oracle
+
+    out = {}
+    plan = [
+        ("er2000_k4_degree_vertex", "er2000", dict(k=4, algorithm="orient", scheme="vertex",
+                                                     criterion="degree"), True),
+        ("planted_allk_pivot_edge", "planted", dict(k=10, algorithm="pivot", scheme="edge",
+                                                      criterion="degeneracy", all_k=True), False),
+        ("planted_allk_pivot_vertex", "planted", dict(k=10, algorithm="pivot", scheme="vertex",
+                                                        criterion="degeneracy", all_k=True), False),
+        ("rmat20_k5_orient_vertex", "rmat20", dict(k=5, algorithm="orient", scheme="vertex",
+                                                     criterion="degeneracy"), False),
+        ("rmat20_k5_orient_edge", "rmat20", dict(k=5, algorithm="orient", scheme="edge",
+                                                   criterion="degeneracy"), False),
+    ]
+    graphs = {}
+    for name, wl, kw, check in plan:
+        try:
+            if wl not in graphs:
+                e = workload_edges(wl)
+                graphs[wl] = (e, kc.from_edges(e, device=local))
+            e, gg = graphs[wl]
+            c = kc.RunConfig(**kw)
+            st = lambda gg=gg, c=c: kc.run_count(gg, c)  # noqa: E731
+            st()
+            r, t = time_steps(st, 2)
+            rec = {"config": kw, "count": str(r.count), "ms_per_step": t / 2,
+                   "cliques_per_s": r.count * 2 / (t / 1e3) if t else None,
+                   "visits": r.load.total, "normalized_max": r.load.normalized_max,
+                   "n": gg.n, "m": gg.m, "d_max": r.d_max}
+            if r.counts:
+                rec["max_k"] = max(r.counts)
+                rec["counts_k10_k30"] = {str(k): str(r.counts.get(k, 0)) for k in (10, 20, 30)}
+            if check:  # bit-exact against the CPU oracle on the same input
+                o = oracle.run_count(oracle.from_edges(e), kw["k"], kw["algorithm"], kw["scheme"],
+                                     kw["criterion"], workers=os.cpu_count() or 1)
+                rec["oracle_match"] = (o.count == r.count and o.visits == r.load.total)
+            out[name] = rec
+        except Exception as exc:  # a side measurement never breaks the headline line
+            out[name] = {"error": str(exc)[:200]}
+    for _, gg in graphs.values():
+        gg.free()
+    return out
 
 
 def roofline(kc, g, cfg, rep, a, local):
