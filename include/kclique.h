@@ -44,6 +44,8 @@ extern "C" {
 #define KC_CRIT_DEGREE 0
 #define KC_CRIT_DEGENERACY 1
 #define KC_CRIT_GIVEN 2 /* use a caller-provided rank permutation */
+#define KC_CRIT_DEGENERACY_EXACT 3 /* the reference's sequential heap order, exactly
+                                      (orientation.py:81-113); slower than the bulk peel */
 
 /* algorithms / schemes (scheduler.py:27-28) */
 #define KC_ALGO_ORIENT 0

@@ -22,7 +22,10 @@ import numpy as np
 
 from . import _lib
 
-CRITERIA = ("degree", "degeneracy")
+# "degeneracy_exact" (extension): the reference's sequential heap order
+# (orientation.py:81-113) reproduced exactly on the GPU -- identical ranks and
+# therefore identical visits; slower than the bulk peel used by "degeneracy".
+CRITERIA = ("degree", "degeneracy", "degeneracy_exact")
 _token = itertools.count(1)
 
 
@@ -118,7 +121,7 @@ def compute_rank(g, criterion: str) -> Ranking:
     rank = np.empty(g.n, dtype=np.int32)
     if g.n:
         _lib.check(_lib.load().kc_dag_download(g.handle, _lib._ptr(rank), None, None, None))
-    degen = int(info.degeneracy) if criterion == "degeneracy" else None
+    degen = int(info.degeneracy) if criterion.startswith("degeneracy") else None
     r = Ranking(rank, criterion, degen, rank_ms=float(info.rank_ms), rounds=int(info.rounds))
     r._graph, r._token = g, tok
     r._dag = OrientedGraph(g, r, info, tok)
@@ -141,7 +144,7 @@ def rank_and_orient(g, criterion: str) -> OrientedGraph:
     if criterion not in CRITERIA:
         raise ValueError(f"unknown orientation criterion: {criterion!r}")
     info, tok = _orient_on_device(g, criterion)
-    degen = int(info.degeneracy) if criterion == "degeneracy" else None
+    degen = int(info.degeneracy) if criterion.startswith("degeneracy") else None
     r = _LazyRanking(g, criterion, degen, float(info.rank_ms), int(info.rounds))
     r._graph, r._token = g, tok
     og = OrientedGraph(g, r, info, tok)
