@@ -55,6 +55,18 @@ def hbm_peak() -> tuple[float, str]:
     return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
+def ncu_traffic(kernel: str = "k_count_warp") -> dict | None:
+    """DRAM bytes per launch of the counting kernel from the committed ncu
+    --set full capture (profiles/r1_traffic.json), or None."""
+    here = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    try:
+        with open(os.path.join(here, "profiles", "r1_traffic.json")) as f:
+            d = json.load(f)
+        return d.get(kernel)
+    except (OSError, ValueError):
+        return None
+
+
 def roofline(g, cfg, rep) -> dict | None:
     c = rep.counters
     if not c or not c.get("kernel_ms"):
@@ -76,6 +88,12 @@ def roofline(g, cfg, rep) -> dict | None:
          "traffic": None,
          "algorithmic": f"{c['extract_bytes']} extraction bytes in {c['kernel_ms']:.3f} ms",
          "peak_source": src}
+    tr = ncu_traffic()
+    if tr:
+        # dram__bytes_read.sum + dram__bytes_write.sum of one captured launch
+        h["traffic"] = tr.get("dram_bytes")
+        a["traffic"] = tr.get("dram_bytes")
+        a["traffic_note"] = tr.get("note")
     main, other = (a, h) if alu_frac >= hbm_frac else (h, a)
     main["kernel"] = "k_count (fused extract + traverse)"
     main["kernel_ms"] = c["kernel_ms"]
