@@ -46,7 +46,9 @@ struct CountParams {
     int t;             // target inside a task
     int all_k;         // pivot all-k
     int split;         // tasks are out-edges of split vertex roots (see kc_do_count)
+    const int32_t *task_w;  // split triples: third vertex w of task (v,u,w), else nullptr
     int32_t *overflow;   // warp kernel: edge tasks with more than kWarpD locals
+    int32_t *overflow_w;  // and their third vertex (triples)
     ull *overflow_n;
     kct::GQueue gq;      // pivot: GPU-wide subtree queue of the warp-tier kernel
     int use_gq;
@@ -116,12 +118,22 @@ __device__ __forceinline__ int smem_find(const int32_t *a, int n, int32_t x) {
     return (lo < n && a[lo] == x) ? lo : -1;
 }
 
+__device__ __forceinline__ bool gl_contains(const int32_t *__restrict__ a, int n, int32_t x) {
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (__ldg(a + mid) < x) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo < n && __ldg(a + lo) == x;
+}
+
 // Returns d (number of locals); fills l2g and (when t >= 2 or pivot) rows.
 // scratch must hold >= dcap int32 (used for the edge scheme's second list).
 template <int BLOCK>
 __device__ int build_task(const CountParams &p, int32_t task, int32_t *l2g, uint32_t *rows,
                           int32_t *scratch, bool need_rows, bool directed, int *s_cnt,
-                          int *s_warp, ull &bytes) {
+                          int *s_warp, ull &bytes, int32_t w3 = -1) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     constexpr int NW = BLOCK / 32;
     int d;
@@ -149,6 +161,8 @@ __device__ int build_task(const CountParams &p, int32_t task, int32_t *l2g, uint
             int i = c + tid;
             int32_t x = i < la ? p.ocol[ab + i] : 0;
             bool f = i < la && smem_find(scratch, lb, x) >= 0;
+            if (w3 >= 0 && f)  // triple (v,u,w): also a out-neighbour of w
+                f = gl_contains(p.ocol + p.orow[w3], int(p.orow[w3 + 1] - p.orow[w3]), x);
             block_append<BLOCK>(f, x, l2g, s_cnt, s_warp);
         }
         d = *s_cnt;
@@ -420,7 +434,7 @@ __global__ void __launch_bounds__(BLOCK) k_count(CountParams p) {
             const int32_t task = p.tasks[s_task];
             const bool need_rows = MODE == MODE_EXTRACT || MODE == MODE_PIVOT || t >= 2;
             d = build_task<BLOCK>(p, task, l2g, rows, scratch, need_rows, directed, &s_cnt, s_warp,
-                                  bytes);
+                                  bytes, p.task_w ? p.task_w[s_task] : -1);
         }
         if (MODE == MODE_EXTRACT) {
             const int W = (d + 31) >> 5, RS = row_stride(W);
@@ -477,15 +491,6 @@ constexpr int kWarpD = 128;
 constexpr int kGqCap = 4096;  // GPU-wide subtree queue slots (pivot)
 constexpr int kSplitD = 32;  // orientation/vertex: roots above this are split into edge items
 
-__device__ __forceinline__ bool gl_contains(const int32_t *__restrict__ a, int n, int32_t x) {
-    int lo = 0, hi = n;
-    while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (__ldg(a + mid) < x) lo = mid + 1;
-        else hi = mid;
-    }
-    return lo < n && __ldg(a + lo) == x;
-}
 
 // warp-level bit matrix of the sub-graph induced by the sorted vertices l2g[0..d)
 // (bitgraph.py:89-111: bit j of row i <=> arc l2g[i] -> l2g[j], or either arc)
@@ -515,7 +520,7 @@ __device__ void warp_rows(const CountParams &p, const int32_t *l2g, int d, uint3
 
 // warp-level K4: locals + bit matrix of one task (d <= kWarpD)
 __device__ int warp_build(const CountParams &p, int32_t task, int32_t *l2g, uint32_t *rows,
-                          bool need_rows, bool directed, ull &bytes) {
+                          bool need_rows, bool directed, ull &bytes, int32_t w3 = -1) {
     const int lane = threadIdx.x & 31;
     int d;
     if (p.scheme == KC_SCHEME_VERTEX) {
@@ -536,7 +541,9 @@ __device__ int warp_build(const CountParams &p, int32_t task, int32_t *l2g, uint
         for (int c = 0; c < la; c += 32) {
             const int i = c + lane;
             const int32_t x = i < la ? p.ocol[ab + i] : 0;
-            const bool f = i < la && gl_contains(p.ocol + bb, lb, x);
+            bool f = i < la && gl_contains(p.ocol + bb, lb, x);
+            if (w3 >= 0 && f)  // triple (v,u,w): also an out-neighbour of w
+                f = gl_contains(p.ocol + p.orow[w3], int(p.orow[w3 + 1] - p.orow[w3]), x);
             const unsigned m = __ballot_sync(kct::FULL, f);
             const int at = d + __popc(m & ((1u << lane) - 1u));
             if (f && at < kWarpD) l2g[at] = x;
@@ -605,9 +612,14 @@ __global__ void __launch_bounds__(BLOCK) k_count_warp(CountParams p) {
         if (i >= ull(p.n_tasks)) break;
         const int32_t task = p.tasks[i];
         const bool need_rows = MODE == MODE_PIVOT || t >= 2;
-        const int d = warp_build(p, task, l2g, rows, need_rows, MODE == MODE_ORIENT, bytes);
+        const int d = warp_build(p, task, l2g, rows, need_rows, MODE == MODE_ORIENT, bytes,
+                                 p.task_w ? p.task_w[i] : -1);
         if (d > D) {  // edge task larger than the warp tier: CTA kernel, next launch
-            if (lane == 0) p.overflow[atomicAdd(p.overflow_n, 1ull)] = task;
+            if (lane == 0) {
+                const ull at = atomicAdd(p.overflow_n, 1ull);
+                p.overflow[at] = task;
+                if (p.task_w) p.overflow_w[at] = p.task_w[i];
+            }
             continue;
         }
         if (p.split) {
@@ -833,6 +845,47 @@ __global__ void k_edge_sizes(const int64_t *__restrict__ orow, const int32_t *__
         for (int i = lane; i < la; i += 32) c += gl_contains(ocol + bb, lb, ocol[ab + i]) ? 1 : 0;
         for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
         if (lane == 0) esize[e] = c;
+    }
+}
+
+__global__ void k_gather_sizes(const int32_t *__restrict__ items, int64_t n,
+                               const int32_t *__restrict__ esize, int32_t *__restrict__ out) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x)
+        out[i] = esize[items[i]];
+}
+
+// triples (e, w) for every w in N+(u) n N+(v) of each big edge item e = (u,v):
+// the level-1 subtrees of the item's tree (warp per item, ascending w)
+__global__ void k_make_triples(const int64_t *__restrict__ orow, const int32_t *__restrict__ ocol,
+                               const int32_t *__restrict__ ocoo, const int32_t *__restrict__ items,
+                               int64_t n, const int32_t *__restrict__ offs,
+                               int32_t *__restrict__ tri_e, int32_t *__restrict__ tri_w) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
+    const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t it = warp; it < n; it += nwarps) {
+        const int32_t e = items[it];
+        const int32_t u = ocoo[e], v = ocol[e];
+        int64_t ab = orow[u], ae = orow[u + 1], bb = orow[v], be = orow[v + 1];
+        if (ae - ab > be - bb) {
+            int64_t t0 = ab, t1 = ae;
+            ab = bb; ae = be; bb = t0; be = t1;
+        }
+        const int la = int(ae - ab), lb = int(be - bb);
+        int at = offs[it];
+        for (int c = 0; c < la; c += 32) {
+            const int i = c + lane;
+            const int32_t x = i < la ? ocol[ab + i] : 0;
+            const bool f = i < la && gl_contains(ocol + bb, lb, x);
+            const unsigned m = __ballot_sync(0xffffffffu, f);
+            if (f) {
+                const int k = at + __popc(m & ((1u << lane) - 1u));
+                tri_e[k] = e;
+                tri_w[k] = x;
+            }
+            at += __popc(m);
+        }
     }
 }
 
@@ -1175,22 +1228,60 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
     // are routed exactly by out-degree: big ones to the CTA kernel on the
     // graph stream, concurrently with the warp kernel on the aux stream.
     const bool edge_like = split || a->scheme == KC_SCHEME_EDGE;
-    DevBuf ovf(4 * size_t(std::max<int64_t>(split ? n_items : n_tasks, 1)));
+    const int64_t n_tri_max = n_items_big * std::max<int64_t>(g->d_max, 1);  // triples bound
+    DevBuf ovf(4 * size_t(std::max<int64_t>(split ? std::max(n_items, n_tri_max) : n_tasks, 1)));
+    DevBuf ovf_w(4 * size_t(std::max<int64_t>(split ? std::max(n_items, n_tri_max) : 1, 1)));
     p.overflow = ovf.as<int32_t>();
+    p.overflow_w = ovf_w.as<int32_t>();
     p.overflow_n = o + 8 + kSmidSlots + 3;
     if (!g->aux) KC_CUDA(cudaStreamCreateWithFlags(&g->aux, cudaStreamNonBlocking));
     KC_CUDA(cudaEventRecord(e_fork, g->stream));
     KC_CUDA(cudaStreamWaitEvent(g->aux, e_fork, 0));
+    DevBuf tri_e, tri_w;
+    int64_t n_tri = 0;
     if (split) {
+        // items with more than kWarpD locals are split once more into triples
+        // (v,u,w), w in N+(v) n N+(u): the level-1 subtrees of item (v,u),
+        // walked with target t-2 after counting w's own visit; u's visit is
+        // added on the host (raw->visits += n_items_big)
         if (n_items_big > 0) {
-            CountParams b = p;
-            b.scheme = KC_SCHEME_EDGE;
-            b.t = t - 1;
-            b.split = 1;
-            b.tasks = items.as<int32_t>();
-            b.n_tasks = n_items_big;
-            b.task_counter = o + 8 + kSmidSlots + 5;
-            launch<MODE_ORIENT>(g, b, 0, keep, g->stream);
+            DevBuf sizes(4 * size_t(n_items_big)), offs(4 * size_t(n_items_big));
+            k_gather_sizes<<<grid_1d(n_items_big, g->num_sms), 256, 0, g->stream>>>(
+                items.as<int32_t>(), n_items_big, g->esize, sizes.as<int32_t>());
+            size_t bytes = 0;
+            KC_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, sizes.as<int32_t>(),
+                                                  offs.as<int32_t>(), int(n_items_big),
+                                                  g->stream));
+            void *tmp = kc_tmp(g, bytes);
+            KC_CUDA(cub::DeviceScan::ExclusiveSum(tmp, bytes, sizes.as<int32_t>(),
+                                                  offs.as<int32_t>(), int(n_items_big),
+                                                  g->stream));
+            int32_t last[2] = {0, 0};
+            KC_CUDA(cudaMemcpyAsync(&last[0], offs.as<int32_t>() + n_items_big - 1, 4,
+                                    cudaMemcpyDeviceToHost, g->stream));
+            KC_CUDA(cudaMemcpyAsync(&last[1], sizes.as<int32_t>() + n_items_big - 1, 4,
+                                    cudaMemcpyDeviceToHost, g->stream));
+            KC_CUDA(cudaStreamSynchronize(g->stream));
+            n_tri = int64_t(last[0]) + last[1];
+            new (&tri_e) DevBuf(4 * size_t(std::max<int64_t>(n_tri, 1)));
+            new (&tri_w) DevBuf(4 * size_t(std::max<int64_t>(n_tri, 1)));
+            if (n_tri > 0) {
+                k_make_triples<<<g->num_sms * 16, 256, 0, g->stream>>>(
+                    g->orow_ptr, g->ocol, g->ocoo, items.as<int32_t>(), n_items_big,
+                    offs.as<int32_t>(), tri_e.as<int32_t>(), tri_w.as<int32_t>());
+                KC_CUDA(cudaGetLastError());
+            }
+        }
+        if (n_tri > 0) {
+            CountParams q = p;
+            q.scheme = KC_SCHEME_EDGE;
+            q.t = t - 2;
+            q.split = 1;
+            q.tasks = tri_e.as<int32_t>();
+            q.task_w = tri_w.as<int32_t>();
+            q.n_tasks = n_tri;
+            q.task_counter = o + 8 + kSmidSlots + 5;
+            launch_warp<MODE_ORIENT>(g, q, keep, g->stream);
         }
         if (n_items - n_items_big > 0) {
             CountParams q = p;
@@ -1229,10 +1320,13 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
         KC_CUDA(cudaMemcpyAsync(&n_ovf, p.overflow_n, 8, cudaMemcpyDeviceToHost, g->stream));
         KC_CUDA(cudaStreamSynchronize(g->stream));
         if (n_ovf > 0) {
+            // in split mode only triples can overflow (items and roots are
+            // routed by exact size); elsewhere only plain edge tasks
             CountParams b = p;
             b.scheme = KC_SCHEME_EDGE;
-            b.t = split ? t - 1 : t;
+            b.t = split ? t - 2 : t;
             b.split = split ? 1 : 0;
+            b.task_w = split ? ovf_w.as<int32_t>() : nullptr;
             b.tasks = ovf.as<int32_t>();
             b.n_tasks = int64_t(n_ovf);
             b.task_counter = o + 8 + kSmidSlots + 4;
@@ -1260,11 +1354,13 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
     raw->word_ops = h[8 + kSmidSlots];
     raw->extract_bytes = h[9 + kSmidSlots];
     for (int i = 0; i < 4; ++i) raw->limbs[i] = h[1 + i];
-    raw->visits = h[5];
+    raw->visits = h[5] + ull(n_items_big);  // u's visit of every item split into triples
     raw->tasks_run = h[6];
     raw->count_ms = ms;
-    if (visits_per_sm)
+    if (visits_per_sm) {
         for (int i = 0; i < n_sm && i < kSmidSlots; ++i) visits_per_sm[i] = h[8 + i];
+        if (n_sm > 0) visits_per_sm[0] += ull(n_items_big);  // see raw->visits
+    }
 }
 
 void kc_do_extract(kc_graph *g, int scheme, int64_t task, int directed, int64_t *l2g,
