@@ -25,6 +25,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <memory>
 #include <vector>
@@ -706,9 +707,12 @@ __global__ void __launch_bounds__(BLOCK) k_count_warp(CountParams p) {
                 // items -- a pusher re-checks `hungry` under the lock, so
                 // leaving never strands an item.
                 const unsigned jitter = (blockIdx.x * 7 + warp * 13) & 127;
+                unsigned backoff = 128;
+                const unsigned long long t_start = kc_globaltimer();
                 for (int spins = 0;; ++spins) {
                     const int sz = q.vol(1);
-                    const bool give_up = sz == 0 && (q.vol(3) == 0 || spins >= 4000);
+                    const bool stale = kc_globaltimer() - t_start > 2000000ull;  // 2 ms idle
+                    const bool give_up = sz == 0 && (q.vol(3) == 0 || stale);
                     if ((sz > 0 || give_up) && atomicCAS(q.ctl, 0, 1) == 0) {
                         __threadfence();
                         const int sz2 = q.vol(1);
@@ -718,7 +722,7 @@ __global__ void __launch_bounds__(BLOCK) k_count_warp(CountParams p) {
                             atomicAdd(q.ctl + 3, 1);
                             break;
                         }
-                        if (q.vol(3) == 0 || spins >= 4000) {
+                        if (q.vol(3) == 0 || stale) {
                             done = 1;
                             atomicSub(q.ctl + 2, 1);
                             q.release();
@@ -726,7 +730,8 @@ __global__ void __launch_bounds__(BLOCK) k_count_warp(CountParams p) {
                         }
                         q.release();
                     }
-                    __nanosleep(128 + jitter);
+                    __nanosleep(backoff + jitter);
+                    backoff = backoff < 16384 ? 2 * backoff : backoff;  // exponential back-off
                 }
             }
             slot = __shfl_sync(kct::FULL, slot, 0);
@@ -735,12 +740,33 @@ __global__ void __launch_bounds__(BLOCK) k_count_warp(CountParams p) {
             // L2-coherent loads (__ldcg): this SM's L1 may hold an older item
             // of the same slot
             const uint32_t *it = q.items + int64_t(slot) * kct::kGItemWords;
-            const int n = int(__ldcg(it)), s0 = int(__ldcg(it + 1)), npv = int(__ldcg(it + 2));
-            for (int i = lane; i < n; i += 32) l2g[i] = int32_t(__ldcg(it + 4 + i));
+            const uint32_t h0 = __ldcg(it);
+            const int s0 = int(__ldcg(it + 1)), npv = int(__ldcg(it + 2));
+            const uint32_t kind = __ldcg(it + 3);
+            const int n = int(h0);
+            if (kind == 1u) SS.srow[lane] = __ldcg(it + 4 + lane);
+            else
+                for (int i = lane; i < n; i += 32) l2g[i] = int32_t(__ldcg(it + 4 + i));
             __syncwarp();
             if (lane == 0) {
                 q.set(1, slot);
+                atomicAdd(q.ctl + 5, 1);  // pops (diagnostics)
                 q.release();
+            }
+            if (kind == 1u) {  // compressed S-tier subtree: no rebuild
+                const uint32_t myrow = SS.srow[lane];
+                const ull wt1 = work;
+                kct::pivot_small(SS.srow, myrow, h0, s0, npv, t, allk, SS.sstk, sink, lane, visits,
+                                 work);
+                (void)wt1;
+                if (lane == 0) {
+                    q.acquire();
+                    atomicSub(q.ctl + 3, 1);
+                    atomicAdd(q.ctl + 2, 1);
+                    q.release();
+                }
+                __syncwarp();
+                continue;
             }
             // the subtree of X depends only on the sub-graph induced by X
             warp_rows(p, l2g, n, rows, false, bytes);
@@ -1208,8 +1234,8 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
     KC_CUDA(cudaEventCreateWithFlags(&e_fork, cudaEventDisableTiming));
     KC_CUDA(cudaEventCreateWithFlags(&e_join, cudaEventDisableTiming));
     KC_CUDA(cudaEventRecord(e0, g->stream));
-    DevBuf gq_items(pivot ? 4 * size_t(kGqCap) * kct::kGItemWords : 4), gq_ctl(16);
-    KC_CUDA(cudaMemsetAsync(gq_ctl.p, 0, 16, g->stream));
+    DevBuf gq_items(pivot ? 4 * size_t(kGqCap) * kct::kGItemWords : 4), gq_ctl(32);
+    KC_CUDA(cudaMemsetAsync(gq_ctl.p, 0, 32, g->stream));
     p.gq.items = gq_items.as<uint32_t>();
     p.gq.ctl = gq_ctl.as<int>();
     p.gq.cap = kGqCap;
@@ -1355,6 +1381,12 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
     raw->extract_bytes = h[9 + kSmidSlots];
     for (int i = 0; i < 4; ++i) raw->limbs[i] = h[1 + i];
     raw->visits = h[5] + ull(n_items_big);  // u's visit of every item split into triples
+    if (p.use_gq && getenv("KC_GQ_DEBUG")) {
+        int c[8] = {0};
+        KC_CUDA(cudaMemcpy(c, gq_ctl.p, 32, cudaMemcpyDeviceToHost));
+        fprintf(stderr, "[kc_gq] pushes=%d pops=%d size=%d hungry=%d busy=%d\n", c[4], c[5], c[1],
+                c[2], c[3]);
+    }
     raw->tasks_run = h[6];
     raw->count_ms = ms;
     if (visits_per_sm) {

@@ -151,6 +151,12 @@ __device__ __forceinline__ int64_t kc_lower_bound_i32(const int32_t *__restrict_
     return lo;
 }
 
+__device__ __forceinline__ unsigned long long kc_globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 __device__ __forceinline__ unsigned kc_smid() {
     unsigned r;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(r));

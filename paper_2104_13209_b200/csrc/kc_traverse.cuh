@@ -414,7 +414,10 @@ constexpr int kLeafCells = kLeafHL * (kLeafHL + 1) / 2;
 // re-checks `hungry` under the lock -- can never strand an item.
 // ---------------------------------------------------------------------------
 constexpr int kGItemMax = 128;
-constexpr int kGItemWords = 4 + kGItemMax;  // [n][s][npv][-][ids]
+constexpr int kGItemWords = 4 + kGItemMax;  // [n | X][s][npv][kind][ids | srow]
+// item kinds: 0 = sorted global vertex ids (the thief rebuilds the induced
+// sub-graph); 1 = compressed S-tier subtree: the 32 compressed rows travel
+// with the set X, so the thief only copies 32 words
 constexpr int kPushMin = 12;      // smaller children are cheaper to walk than to rebuild
 constexpr int kPushCooldown = 256;  // child decisions between two hand-overs of one warp
 struct GQueue {
@@ -479,9 +482,21 @@ struct PivotLeafSink {
         if (lane == 0) {
             __threadfence();
             gq->set(1, slot + 1);
+            atomicAdd(gq->ctl + 4, 1);  // pushes (diagnostics)
             gq->release();
         }
         __syncwarp();
+    }
+    // compressed S-tier child X over the compressed rows srow
+    __device__ __forceinline__ bool push_compressed(const uint32_t *srow, uint32_t X, int s,
+                                                    int npv, int lane) const {
+        const int slot = reserve(lane);
+        if (slot < 0) return false;
+        uint32_t *it = gq->items + int64_t(slot) * kGItemWords;
+        it[4 + lane] = srow[lane];
+        if (lane == 0) it[3] = 1u;
+        publish(slot, int(X), s, npv, lane);
+        return true;
     }
     // S-tier child X (compressed ids; map = compressed -> local, nullptr = identity)
     __device__ __forceinline__ bool push_small(uint32_t X, const int *map, int s, int npv,
@@ -489,6 +504,7 @@ struct PivotLeafSink {
         const int slot = reserve(lane);
         if (slot < 0) return false;
         uint32_t *ids = gq->items + int64_t(slot) * kGItemWords + 4;
+        if (lane == 0) ids[-1] = 0u;  // kind 0
         if ((X >> lane) & 1u) {
             const int local = map ? map[lane] : lane;
             ids[__popc(X & ((1u << lane) - 1u))] = uint32_t(l2g[local]);
@@ -555,7 +571,7 @@ __device__ __forceinline__ void donate_bottom(const uint32_t *srow, const int *m
         ++uvis;
         return;
     }
-    if (__popc(X) >= kPushMin && sink.push_small(X, map, sj + 1, np2, lane)) {
+    if (__popc(X) >= kPushMin && sink.push_compressed(srow, X, sj + 1, np2, lane)) {
         ++uvis;
         return;
     }
@@ -823,6 +839,7 @@ __device__ __forceinline__ bool push_large(const PivotLeafSink &sink, const Set<
     if (slot < 0) return false;
     const int n = compact<WPL>(X, list, lane);
     uint32_t *ids = sink.gq->items + int64_t(slot) * kGItemWords + 4;
+    if (lane == 0) ids[-1] = 0u;  // kind 0
     for (int i = lane; i < n; i += 32) ids[i] = uint32_t(sink.l2g[list[i]]);
     sink.publish(slot, n, s, npv, lane);
     return true;
