@@ -327,13 +327,20 @@ __device__ __forceinline__ void pairs_small(const uint32_t *srow, uint32_t C, in
         const int xs = __popc(m);
         visits += ull(1 + xs);
         work += ull(1 + xs);
-        ull a = 0;
+        // two members per trip: independent shared loads in flight, 32-bit sums
+        unsigned a0 = 0, a1 = 0;
         while (m) {
-            const int x = __ffs(m) - 1;
+            const int x0 = __ffs(m) - 1;
             m &= m - 1u;
-            a += __popc(cm & srow[x]);
+            const uint32_t r0 = srow[x0];
+            if (m) {
+                const int x1 = __ffs(m) - 1;
+                m &= m - 1u;
+                a1 += __popc(cm & srow[x1]);
+            }
+            a0 += __popc(cm & r0);
         }
-        acc += a;
+        acc += ull(a0 + a1);
     }
 }
 
