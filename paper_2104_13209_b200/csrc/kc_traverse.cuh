@@ -852,6 +852,62 @@ __device__ __forceinline__ bool push_large(const PivotLeafSink &sink, const Set<
     return true;
 }
 
+// L-tier bottom-of-stack donation: find the shallowest stored frame sf in
+// [s0, s_top) with a pending branch v, and hand v's child set to the queue as
+// a global-id item (same rules as donate_bottom for the S-tier).  Frames keep
+// (C, P, piv, npv, cursor); advancing the cursor to v marks v as taken.
+template <int WPL>
+__device__ __forceinline__ void donate_bottom_L(const uint32_t *__restrict__ rows, int RS, int W,
+                                                int t, bool allk, const Frames &F, int s0,
+                                                int s_top, int *list, const PivotLeafSink &sink,
+                                                int lane, ull &visits) {
+    const int PO = 32 * WPL, SC = 64 * WPL;
+    for (int sf = s0; sf < s_top; ++sf) {
+        uint32_t *f = F.at(sf);
+        const Set<WPL> Cf = load_set<WPL>(f, lane), Pf = load_set<WPL>(f + PO, lane);
+        const int piv = int(f[SC]), npv = int(f[SC + 1]), c = int(f[SC + 2]);
+        Set<WPL> R;
+#pragma unroll
+        for (int p = 0; p < WPL; ++p) R.w[p] = Pf.w[p] & above_mask(p * 32 + lane, c);
+        if (!allk && sf + 1 - t > npv) restrict_to(R, piv, lane);
+        const int v = next_bit<WPL>(R, lane);
+        if (v < 0) continue;
+        const int np2 = npv + (v == piv ? 1 : 0);
+        if (!allk && sf + 1 - t > np2) {  // pruned (not a visit): just take it
+            __syncwarp();
+            if (lane == 0) f[SC + 2] = uint32_t(v);
+            __syncwarp();
+            return;
+        }
+        Set<WPL> X;
+        const uint32_t *rv = rows + v * RS;
+#pragma unroll
+        for (int p = 0; p < WPL; ++p) {
+            const int w = p * 32 + lane;
+            X.w[p] = w < W ? (Cf.w[p] & rv[w] & ~(Pf.w[p] & below_mask(w, v))) : 0u;
+        }
+        const int n = warp_count<WPL>(X);
+        const bool dead = !allk && sf + 2 - t > np2 + 1;
+        bool taken = false;
+        if (n == 0) {
+            if ((allk || sf + 1 >= t) && lane == 0) sink.add(sf + 1, np2);
+            taken = true;
+        } else if (dead) {
+            taken = true;
+        } else if (n >= kPushMin && n <= kGItemMax) {
+            taken = push_large<WPL>(sink, X, list, sf + 1, np2, lane);
+        }
+        if (taken) {
+            if (lane == 0) {
+                ++visits;
+                f[SC + 2] = uint32_t(v);
+            }
+            __syncwarp();
+        }
+        return;  // only the shallowest pending branch is considered
+    }
+}
+
 // Walk the subtree of a fresh child set C (nonempty, not dead) at frame s0
 // with pivot count npv (engine_pivot.py:117-233 from that node down).
 template <int WPL>
@@ -918,9 +974,18 @@ __device__ void pivot_from(const uint32_t *__restrict__ rows, int RS, int W, int
             if (!allk && s + 2 - t > np2 + 1) continue;
             {
                 const int nx = warp_count<WPL>(X);
-                if (WPL == 1 && sink.want_push(nx, lane) &&
-                    push_large<WPL>(sink, X, list, s + 1, np2, lane))
-                    continue;
+                if (WPL == 1 && sink.want_push(nx, lane)) {
+                    // donate the shallowest pending branch if there is one
+                    // below this frame, else this child
+                    if (s > s0) {
+                        if (lane == 0) F.at(s)[SC + 2] = uint32_t(v);  // cursor of the top frame
+                        __syncwarp();
+                        donate_bottom_L<WPL>(rows, RS, W, t, allk, F, s0, s, list, sink, lane,
+                                             visits);
+                    } else if (push_large<WPL>(sink, X, list, s + 1, np2, lane)) {
+                        continue;
+                    }
+                }
                 if (q && nx > 32 && steal_push<WPL>(*q, X, s + 1, np2, lane)) continue;
             }
             if (pivot_try_small<WPL>(rows, RS, W, X, s + 1, np2, t, allk, list, SS, sink, lane,
