@@ -1270,7 +1270,20 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
         // (v,u,w), w in N+(v) n N+(u): the level-1 subtrees of item (v,u),
         // walked with target t-2 after counting w's own visit; u's visit is
         // added on the host (raw->visits += n_items_big)
-        if (n_items_big > 0) {
+        // triples re-intersect their item's lists once per w: worth it only
+        // for deep trees (t >= 6, i.e. k >= 7); shallower runs keep big
+        // items in the CTA-cooperative kernel
+        if (n_items_big > 0 && t < 6) {
+            CountParams b = p;
+            b.scheme = KC_SCHEME_EDGE;
+            b.t = t - 1;
+            b.split = 1;
+            b.tasks = items.as<int32_t>();
+            b.n_tasks = n_items_big;
+            b.task_counter = o + 8 + kSmidSlots + 6;
+            launch<MODE_ORIENT>(g, b, 0, keep, g->stream);
+        }
+        if (n_items_big > 0 && t >= 6) {
             DevBuf sizes(4 * size_t(n_items_big)), offs(4 * size_t(n_items_big));
             k_gather_sizes<<<grid_1d(n_items_big, g->num_sms), 256, 0, g->stream>>>(
                 items.as<int32_t>(), n_items_big, g->esize, sizes.as<int32_t>());
@@ -1380,7 +1393,8 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
     raw->word_ops = h[8 + kSmidSlots];
     raw->extract_bytes = h[9 + kSmidSlots];
     for (int i = 0; i < 4; ++i) raw->limbs[i] = h[1 + i];
-    raw->visits = h[5] + ull(n_items_big);  // u's visit of every item split into triples
+    const ull tri_items = (split && t >= 6) ? ull(n_items_big) : 0ull;
+    raw->visits = h[5] + tri_items;  // u's visit of every item split into triples
     if (p.use_gq && getenv("KC_GQ_DEBUG")) {
         int c[8] = {0};
         KC_CUDA(cudaMemcpy(c, gq_ctl.p, 32, cudaMemcpyDeviceToHost));
@@ -1391,7 +1405,7 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
     raw->count_ms = ms;
     if (visits_per_sm) {
         for (int i = 0; i < n_sm && i < kSmidSlots; ++i) visits_per_sm[i] = h[8 + i];
-        if (n_sm > 0) visits_per_sm[0] += ull(n_items_big);  // see raw->visits
+        if (n_sm > 0) visits_per_sm[0] += tri_items;  // see raw->visits
     }
 }
 

@@ -213,6 +213,29 @@ __device__ __forceinline__ void score_pairs(const uint32_t *__restrict__ rows, i
                 m &= m - 1u;
                 a += __popc(cm & rows[x * RS]);
             }
+        } else if (WPL == 1 && W <= 4) {
+            // rows of at most 4 words (the warp tier): C & row v in registers,
+            // fully unrolled 3-way AND + POPC per member x
+            uint32_t cm[4];
+#pragma unroll
+            for (int w = 0; w < 4; ++w) cm[w] = w < W ? (cbuf[w] & rv[w]) : 0u;
+            unsigned a32 = 0;
+#pragma unroll
+            for (int w = 0; w < 4; ++w) {
+                uint32_t m = cm[w];
+                x_seen += __popc(m);
+                while (m) {
+                    const int x = (w << 5) + __ffs(m) - 1;
+                    m &= m - 1u;
+                    const uint32_t *rx = rows + x * RS;
+                    unsigned c = __popc(cm[0] & rx[0]);
+                    if (W > 1) c += __popc(cm[1] & rx[1]);
+                    if (W > 2) c += __popc(cm[2] & rx[2]);
+                    if (W > 3) c += __popc(cm[3] & rx[3]);
+                    a32 += c;
+                }
+            }
+            a += a32;
         } else if (WPL == 1) {
             // word-sparse: only words where C & row v is nonzero matter
             uint32_t nzm = 0;
