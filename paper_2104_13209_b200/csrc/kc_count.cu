@@ -558,7 +558,7 @@ __device__ int warp_build(const CountParams &p, int32_t task, int32_t *l2g, uint
     return d;
 }
 
-template <int BLOCK, int MODE>
+template <int BLOCK, int MODE, bool GQ>
 __global__ void __launch_bounds__(BLOCK) k_count_warp(CountParams p) {
     constexpr int NW = BLOCK / 32;
     constexpr int D = kWarpD, WPL = 1;
@@ -592,7 +592,7 @@ __global__ void __launch_bounds__(BLOCK) k_count_warp(CountParams p) {
     sink.whist = whist;
     sink.g_hist = p.hist;
     sink.L = p.hist_dim;
-    sink.gq = (MODE == MODE_PIVOT && p.use_gq) ? &p.gq : nullptr;
+    sink.gq = (GQ && MODE == MODE_PIVOT) ? &p.gq : nullptr;  // compile-time off when !GQ
     sink.l2g = l2g;
     sink.hc = s_hc + 2 * warp;
     for (int i = lane; i < hist_cells; i += 32) whist[i] = 0;
@@ -689,7 +689,7 @@ __global__ void __launch_bounds__(BLOCK) k_count_warp(CountParams p) {
         work = wt0 + (work - wt0) * ull(W);
         __syncwarp();
     }
-    if (MODE == MODE_PIVOT && sink.gq) {
+    if (GQ && MODE == MODE_PIVOT) {
         // task queue drained: serve subtrees handed over by busy warps
         const kct::GQueue &q = p.gq;
         if (lane == 0) {
@@ -1098,7 +1098,8 @@ void launch_warp(kc_graph *g, CountParams &p, Keep &keep, cudaStream_t stream) {
     int nsm = std::min(need, 8);
     p.nsm_frames = nsm;
     const size_t smem = 4 * size_t(NW) * (fixed + size_t(nsm) * p.fw) + 64;
-    auto kern = k_count_warp<kBlock, MODE>;
+    auto kern = (MODE == MODE_PIVOT && p.use_gq) ? k_count_warp<kBlock, MODE, true>
+                                                 : k_count_warp<kBlock, MODE, false>;
     KC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     int per_sm = 0;
     KC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBlock, smem));

@@ -450,6 +450,7 @@ constexpr int kGItemWords = 4 + kGItemMax;  // [n | X][s][npv][kind][ids | srow]
 // with the set X, so the thief only copies 32 words
 constexpr int kPushMin = 12;      // smaller children are cheaper to walk than to rebuild
 constexpr int kPushCooldown = 256;  // child decisions between two hand-overs of one warp
+constexpr int kPushRoom = 4;        // hand over only where >= 4 levels remain to target t
 struct GQueue {
     uint32_t *items;  // cap x kGItemWords
     int *ctl;         // [0] lock [1] size [2] hungry [3] busy
@@ -477,8 +478,9 @@ struct PivotLeafSink {
     // uniform: should a child of n members be handed to a hungry warp?
     // Rate-limited: at most one hand-over per kPushCooldown decisions, so a
     // donor keeps doing its own work and thieves get substantial subtrees.
-    __device__ __forceinline__ bool want_push(int n, int lane) const {
+    __device__ __forceinline__ bool want_push(int n, int room, int lane) const {
         if (!gq || n < kPushMin || n > kGItemMax) return false;
+        if (room < kPushRoom) return false;  // shallow remaining tree: cheaper to walk
         if (lane == 0 && --hc[0] <= 0) {
             hc[0] = kPushCooldown;
             hc[1] = gq->vol(2);
@@ -650,7 +652,7 @@ __device__ void pivot_small(const uint32_t *srow, uint32_t myrow, uint32_t C, in
             // GPU-wide work sharing: while some warp is hungry, donate the
             // SHALLOWEST pending branch (the biggest subtree this warp still
             // owns), classic work stealing from the bottom of the stack
-            if (sink.gq && s > s0 && sink.want_push(kPushMin, lane))
+            if (sink.gq && s > s0 && sink.want_push(kPushMin, allk ? 1 << 20 : t - s0, lane))
                 donate_bottom(srow, map, s - s0, s0, t, allk, fC, fP, fR, fPN, sink, lane, uvis);
             if (lane == s - s0) {
                 fC = C;
@@ -997,7 +999,7 @@ __device__ void pivot_from(const uint32_t *__restrict__ rows, int RS, int W, int
             if (!allk && s + 2 - t > np2 + 1) continue;
             {
                 const int nx = warp_count<WPL>(X);
-                if (WPL == 1 && sink.want_push(nx, lane)) {
+                if (WPL == 1 && sink.want_push(nx, allk ? 1 << 20 : t - s0, lane)) {
                     // donate the shallowest pending branch if there is one
                     // below this frame, else this child
                     if (s > s0) {
