@@ -354,7 +354,7 @@ __device__ void pivot_task(const CountParams &p, const uint32_t *rows, int d, ui
 enum Mode { MODE_ORIENT = 0, MODE_PIVOT = 1, MODE_EXTRACT = 2 };
 constexpr int kStealCap = 16;  // pivot work-sharing stack slots per CTA
 
-template <int BLOCK, int MODE, int WPL>
+template <int BLOCK, int MODE, int WPL, bool GQ = false>
 __global__ void __launch_bounds__(BLOCK) k_count(CountParams p) {
     constexpr int NW = BLOCK / 32;
     extern __shared__ __align__(16) unsigned char smem[];
@@ -405,7 +405,7 @@ __global__ void __launch_bounds__(BLOCK) k_count(CountParams p) {
     sink.whist = whist;
     sink.g_hist = p.hist;
     sink.L = p.hist_dim;
-    sink.gq = (MODE == MODE_PIVOT && p.use_gq) ? &p.gq : nullptr;
+    sink.gq = (GQ && MODE == MODE_PIVOT) ? &p.gq : nullptr;  // compile-time off when !GQ
     sink.l2g = l2g;
     sink.hc = s_hc + 2 * warp;
     if ((tid & 31) == 0) {
@@ -1062,7 +1062,8 @@ void launch_wpl(kc_graph *g, CountParams &p, int grid_override, Keep &keep,
     p.nsm_frames = nsm;
     const size_t smem = total(nsm, p.rows_in_smem);
     KC_REQUIRE(smem <= size_t(kSmemMax), KC_ENOMEM, "per-task scratch exceeds shared memory");
-    auto kern = k_count<kBlock, MODE, WPL>;
+    auto kern = (MODE == MODE_PIVOT && p.use_gq) ? k_count<kBlock, MODE, WPL, true>
+                                                 : k_count<kBlock, MODE, WPL, false>;
     KC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     int per_sm = 0;
     KC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBlock, smem));
@@ -1240,12 +1241,10 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
     p.gq.items = gq_items.as<uint32_t>();
     p.gq.ctl = gq_ctl.as<int>();
     p.gq.cap = kGqCap;
-    // experimental (round 1): GPU-wide subtree hand-over, opt-in via KC_GQ=1 --
-    // it is exact but does not yet move the L-tier giant subtrees and its
-    // polling costs more than it saves on RMAT
+    // GPU-wide subtree hand-over for the pivot engine (KC_GQ=0 turns it off)
     static const bool gq_on = [] {
         const char *e = getenv("KC_GQ");
-        return e && e[0] == '1';
+        return !(e && e[0] == '0');  // on unless KC_GQ=0
     }();
     p.use_gq = pivot && gq_on ? 1 : 0;
     Keep keep;
