@@ -475,9 +475,7 @@ __global__ void __launch_bounds__(BLOCK) k_count(CountParams p) {
     __syncthreads();
     if (MODE == MODE_PIVOT) sink.flush(tid & 31);
     if (sink.gq && (tid & 31) == 0) {
-        p.gq.acquire();
-        atomicSub(p.gq.ctl + 3, 1);
-        p.gq.release();
+        atomicSub(p.gq.ctl + 3, 1);  // no longer busy (pushed items are drained by thieves)
     }
     if (MODE != MODE_EXTRACT) flush_block<BLOCK>(p, acc, visits, tasks, work, bytes, s_red);
 }
@@ -692,46 +690,57 @@ __global__ void __launch_bounds__(BLOCK) k_count_warp(CountParams p) {
     if (GQ && MODE == MODE_PIVOT) {
         // task queue drained: serve subtrees handed over by busy warps
         const kct::GQueue &q = p.gq;
-        if (lane == 0) {
-            q.acquire();
-            atomicSub(q.ctl + 3, 1);
+        if (lane == 0) {  // busy -> hungry (atomics only: no lock storm at the tail)
             atomicAdd(q.ctl + 2, 1);
-            q.release();
+            atomicSub(q.ctl + 3, 1);
         }
         for (;;) {
             int slot = -1, done = 0;
             if (lane == 0) {
                 // Poll without the lock; take it with a single try (no
                 // spinning on it: a pusher must never queue behind hundreds
-                // of hungry warps).  Give the SM back after ~1 ms without
-                // items -- a pusher re-checks `hungry` under the lock, so
-                // leaving never strands an item.
+                // of hungry warps); exponential back-off between polls.
                 const unsigned jitter = (blockIdx.x * 7 + warp * 13) & 127;
                 unsigned backoff = 128;
                 const unsigned long long t_start = kc_globaltimer();
-                for (int spins = 0;; ++spins) {
+                for (;;) {
                     const int sz = q.vol(1);
-                    const bool stale = kc_globaltimer() - t_start > 2000000ull;  // 2 ms idle
-                    const bool give_up = sz == 0 && (q.vol(3) == 0 || stale);
-                    if ((sz > 0 || give_up) && atomicCAS(q.ctl, 0, 1) == 0) {
-                        __threadfence();
-                        const int sz2 = q.vol(1);
-                        if (sz2 > 0) {
-                            slot = sz2 - 1;  // lock kept while the item is copied out
-                            atomicSub(q.ctl + 2, 1);
-                            atomicAdd(q.ctl + 3, 1);
-                            break;
-                        }
-                        if (q.vol(3) == 0 || stale) {
-                            done = 1;
-                            atomicSub(q.ctl + 2, 1);
+                    if (sz > 0) {
+                        if (atomicCAS(q.ctl, 0, 1) == 0) {  // single try, never spin on it
+                            __threadfence();
+                            const int sz2 = q.vol(1);
+                            if (sz2 > 0) {
+                                slot = sz2 - 1;  // lock kept while the item is copied out
+                                atomicSub(q.ctl + 2, 1);
+                                atomicAdd(q.ctl + 3, 1);
+                                break;
+                            }
                             q.release();
-                            break;
                         }
+                    } else if (q.vol(6)) {
+                        // closed: nothing can be pushed any more, leave without the lock
+                        atomicSub(q.ctl + 2, 1);
+                        done = 1;
+                        break;
+                    } else if (q.vol(3) == 0) {
+                        // nobody busy: the first warp to see it under the lock closes
+                        // the queue (pushers refuse once closed), everyone else leaves
+                        if (atomicCAS(q.ctl, 0, 1) == 0) {
+                            __threadfence();
+                            if (q.vol(1) == 0 && q.vol(3) == 0) q.set(6, 1);
+                            q.release();
+                        }
+                    } else if (kc_globaltimer() - t_start > 500000ull) {  // 0.5 ms idle
+                        // give the SM back; the lock orders this with pushers'
+                        // `hungry` check, so no item can be stranded
+                        q.acquire();
+                        atomicSub(q.ctl + 2, 1);
                         q.release();
+                        done = 1;
+                        break;
                     }
                     __nanosleep(backoff + jitter);
-                    backoff = backoff < 16384 ? 2 * backoff : backoff;  // exponential back-off
+                    backoff = backoff < 8192 ? 2 * backoff : backoff;  // exponential back-off
                 }
             }
             slot = __shfl_sync(kct::FULL, slot, 0);
@@ -760,10 +769,8 @@ __global__ void __launch_bounds__(BLOCK) k_count_warp(CountParams p) {
                                  work);
                 (void)wt1;
                 if (lane == 0) {
-                    q.acquire();
-                    atomicSub(q.ctl + 3, 1);
                     atomicAdd(q.ctl + 2, 1);
-                    q.release();
+                    atomicSub(q.ctl + 3, 1);
                 }
                 __syncwarp();
                 continue;
@@ -788,10 +795,8 @@ __global__ void __launch_bounds__(BLOCK) k_count_warp(CountParams p) {
             }
             work = wt0 + (work - wt0) * ull(W);
             if (lane == 0) {
-                q.acquire();
-                atomicSub(q.ctl + 3, 1);
                 atomicAdd(q.ctl + 2, 1);
-                q.release();
+                atomicSub(q.ctl + 3, 1);
             }
             __syncwarp();
         }

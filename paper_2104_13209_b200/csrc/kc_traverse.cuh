@@ -453,7 +453,7 @@ constexpr int kPushCooldown = 256;  // child decisions between two hand-overs of
 constexpr int kPushRoom = 4;        // hand over only where >= 4 levels remain to target t
 struct GQueue {
     uint32_t *items;  // cap x kGItemWords
-    int *ctl;         // [0] lock [1] size [2] hungry [3] busy
+    int *ctl;         // [0] lock [1] size [2] hungry [3] busy [4] pushes [5] pops [6] closed
     int cap;
     __device__ __forceinline__ void acquire() const {
         while (atomicCAS(ctl, 0, 1) != 0) __nanosleep(64);
@@ -498,7 +498,7 @@ struct PivotLeafSink {
             gq->acquire();
             // only while more warps are hungry than items are waiting
             const int sz = gq->vol(1);
-            if (sz < gq->cap && sz < gq->vol(2)) slot = sz;
+            if (!gq->vol(6) && sz < gq->cap && sz < gq->vol(2)) slot = sz;  // [6]: closed
             else gq->release();
         }
         return __shfl_sync(0xffffffffu, slot, 0);
