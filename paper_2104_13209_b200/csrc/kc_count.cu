@@ -730,7 +730,7 @@ __global__ void __launch_bounds__(BLOCK) k_count_warp(CountParams p) {
                             if (q.vol(1) == 0 && q.vol(3) == 0) q.set(6, 1);
                             q.release();
                         }
-                    } else if (kc_globaltimer() - t_start > 500000ull) {  // 0.5 ms idle
+                    } else if (kc_globaltimer() - t_start > 20000000ull) {  // 20 ms idle
                         // give the SM back; the lock orders this with pushers'
                         // `hungry` check, so no item can be stranded
                         q.acquire();
