@@ -182,10 +182,17 @@ def run_ours(a):
     import torch.distributed as dist
 
     world, rank, local = dist_env()
+    # one process per GPU; KC_DIST_BACKEND=gloo + fewer GPUs than ranks lets the
+    # N>1 path run on a 1-GPU box (ranks share devices) for testing
+    backend = os.environ.get("KC_DIST_BACKEND", "nccl")
+    local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     os.environ["KC_DEVICE"] = str(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
 
     import paper_2104_13209_b200 as kc
     from paper_2104_13209_b200 import _lib
@@ -208,12 +215,20 @@ def run_ours(a):
     rep = None
     for _ in range(max(a.warmup, 0)):
         rep = step()
-    n_launch, launch_names = count_kernel_launches(step) if rank == 0 else (None, {})
+    # every rank runs the profiled step: it contains the all-reduce at N>1
+    n_launch, launch_names = count_kernel_launches(step)
 
     def barrier():
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        """device times: the job's time is the slowest rank's"""
+        dev = f"cuda:{local}" if backend == "nccl" else "cpu"
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
 
     def time_steps(fn, n):
         """n steps timed with events on the library stream, L2 flushed between."""
@@ -231,9 +246,7 @@ def run_ours(a):
         barrier()
         tot = float(sum(s0.elapsed_time(s1) for s0, s1 in evs))
         if world > 1:
-            tt = torch.tensor([tot], dtype=torch.float64, device=f"cuda:{local}")
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            tot = float(tt.item())
+            tot = max_over_ranks(tot)
         return r, tot
 
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
@@ -255,9 +268,7 @@ def run_ours(a):
     ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     total_ms = float(sum(ms))
     if world > 1:
-        t = torch.tensor([total_ms], dtype=torch.float64, device=f"cuda:{local}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+        total_ms = max_over_ranks(total_ms)
     count = rep.count
     value = count * a.steps / (total_ms / 1e3)
 
@@ -283,9 +294,7 @@ def run_ours(a):
         torch.cuda.synchronize()
         e_ms = (time.perf_counter() - t0) * 1e3
         if world > 1:
-            t = torch.tensor([e_ms], dtype=torch.float64, device=f"cuda:{local}")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e_ms = float(t.item())
+            e_ms = max_over_ranks(e_ms)
         e2e = {"value": count * a.steps / (e_ms / 1e3), "unit": "k-cliques/s",
                "ms_per_step": e_ms / a.steps, "h2d_bytes_per_step": int(edges.nbytes),
                "d2h_bytes_per_step": int(d2h), "timer": "host wall clock, synced"}
