@@ -155,11 +155,9 @@ __global__ void k_orient_flags(const int32_t *__restrict__ col, const int32_t *_
 // barrier ending step p+1, which no thread passes before finishing its
 // reads).  All control values are therefore identical in every thread.
 // ctl: [0..2] cnt, [3..5] mn, [6] degeneracy, [7] rounds.
-constexpr int kSmallFrontier = 2048;  // rounds this small run inside CTA 0 (no grid barrier)
-
 __global__ void k_peel_coop(const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
                             int64_t n, int32_t *__restrict__ deg, int32_t *__restrict__ round_of,
-                            int32_t *__restrict__ order, int32_t *ctl, int64_t *st) {
+                            int32_t *__restrict__ order, int32_t *ctl) {
     cg::grid_group grid = cg::this_grid();
     const int64_t gtid = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
     const int64_t gsz = int64_t(gridDim.x) * blockDim.x;
@@ -216,50 +214,6 @@ __global__ void k_peel_coop(const int64_t *__restrict__ row_ptr, const int32_t *
         tail = end;
         degen = level > degen ? level : degen;
         while (end > head) {
-            if (end - head <= kSmallFrontier) {
-                // Small rounds: CTA 0 peels them alone with block barriers until
-                // the level is exhausted or the frontier grows; the other CTAs
-                // wait at the grid barrier.  Same rounds, same order.
-                if (blockIdx.x == 0) {
-                    __shared__ int s_next;
-                    const int bwarp = threadIdx.x >> 5, bwarps = blockDim.x >> 5;
-                    int64_t h = head, e = end, tl = tail;
-                    int32_t r = round;
-                    while (e > h && e - h <= kSmallFrontier) {
-                        if (threadIdx.x == 0) s_next = 0;
-                        __syncthreads();
-                        for (int64_t i = h + bwarp; i < e; i += bwarps) {
-                            const int32_t v = order[i];
-                            if (lane == 0) round_of[v] = r;
-                            for (int64_t q = row_ptr[v] + lane; q < row_ptr[v + 1]; q += 32) {
-                                const int32_t w = col[q];
-                                if (round_of[w] >= 0) continue;
-                                const int32_t old = atomicSub(&deg[w], 1);
-                                if (old == level + 1) order[tl + atomicAdd(&s_next, 1)] = w;
-                            }
-                        }
-                        __syncthreads();
-                        h = e;
-                        e = tl + s_next;
-                        tl = e;
-                        ++r;
-                        __syncthreads();
-                    }
-                    if (threadIdx.x == 0) {
-                        st[0] = h;
-                        st[1] = e;
-                        st[2] = tl;
-                        st[3] = r;
-                    }
-                }
-                grid.sync();
-                volatile int64_t *vst = st;
-                head = vst[0];
-                end = vst[1];
-                tail = vst[2];
-                round = int32_t(vst[3]);
-                continue;
-            }
             // mark + relax step: warp per frontier vertex marks it removed and
             // decrements its not-yet-removed neighbours; one that crosses
             // level+1 -> level joins the next round's frontier.  Decrementing
@@ -570,7 +524,6 @@ static void degeneracy_rank(kc_graph *g, int64_t *degeneracy, int64_t *rounds_ou
     int32_t *round_of = kc_alloc<int32_t>(n, g->stream);
     int32_t *order = kc_alloc<int32_t>(n, g->stream);
     int32_t *ctl = kc_alloc<int32_t>(8, g->stream);
-    int64_t *st = kc_alloc<int64_t>(4, g->stream);
     // one 1024-thread CTA per SM: grid barriers cost grow with the CTA count
     constexpr int kPeelThreads = 1024;
     int per_sm = 0;
@@ -583,7 +536,7 @@ static void degeneracy_rank(kc_graph *g, int64_t *degeneracy, int64_t *rounds_ou
     const int32_t *cl = g->col;
     int64_t nn = n;
     void *args[] = {(void *)&rp, (void *)&cl, (void *)&nn, (void *)&deg, (void *)&round_of,
-                    (void *)&order, (void *)&ctl, (void *)&st};
+                    (void *)&order, (void *)&ctl};
     KC_CUDA(cudaLaunchCooperativeKernel((void *)k_peel_coop, dim3(grid), dim3(kPeelThreads), args,
                                         0, g->stream));
     int32_t h[8] = {0};
@@ -607,7 +560,6 @@ static void degeneracy_rank(kc_graph *g, int64_t *degeneracy, int64_t *rounds_ou
     kc_free(round_of, g->stream);
     kc_free(order, g->stream);
     kc_free(ctl, g->stream);
-    kc_free(st, g->stream);
     *degeneracy = h[6];
     *rounds_out = round;
 }
