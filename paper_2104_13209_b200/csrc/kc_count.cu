@@ -82,6 +82,11 @@ struct CountParams {
 };
 
 __host__ __device__ __forceinline__ int row_stride(int W) { return W | 1; }
+// warp tier, orientation: rows of 2..4 words padded to 16 bytes so the
+// last-two-levels loop reads a row with one 128-bit load (kc_traverse.cuh)
+__host__ __device__ __forceinline__ int warp_row_stride(int W, bool orient) {
+    return (orient && W >= 2 && W <= 4) ? 4 : row_stride(W);
+}
 
 // ---------------------------------------------------------------------------
 // K4: locals + bit matrix
@@ -496,7 +501,7 @@ constexpr int kSplitD = 32;  // orientation/vertex: roots above this are split i
 __device__ void warp_rows(const CountParams &p, const int32_t *l2g, int d, uint32_t *rows,
                           bool directed, ull &bytes) {
     const int lane = threadIdx.x & 31;
-    const int W = (d + 31) >> 5, RS = row_stride(W);
+    const int W = (d + 31) >> 5, RS = warp_row_stride(W, directed);
     for (int i = lane; i < d * RS; i += 32) rows[i] = 0u;
     __syncwarp();
     const int32_t lo_id = l2g[0], hi_id = l2g[d - 1];
@@ -634,7 +639,7 @@ __global__ void __launch_bounds__(BLOCK) k_count_warp(CountParams p) {
             if (lane == 0) acc += t == 0 ? 1ull : ull(d);
             continue;
         }
-        const int W = (d + 31) >> 5, RS = row_stride(W);
+        const int W = (d + 31) >> 5, RS = warp_row_stride(W, MODE == MODE_ORIENT);
         const uint32_t all = d >= 32 ? kct::FULL : ((1u << d) - 1u);
         const ull wt0 = work;  // units -> §8(d) word-ops of this task at the end
         if (MODE == MODE_ORIENT) {

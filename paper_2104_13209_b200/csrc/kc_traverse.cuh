@@ -220,19 +220,34 @@ __device__ __forceinline__ void score_pairs(const uint32_t *__restrict__ rows, i
 #pragma unroll
             for (int w = 0; w < 4; ++w) cm[w] = w < W ? (cbuf[w] & rv[w]) : 0u;
             unsigned a32 = 0;
+            if (RS == 4) {  // 16-byte rows (warp tier, orientation): one LDS.128 per member
 #pragma unroll
-            for (int w = 0; w < 4; ++w) {
-                uint32_t m = cm[w];
-                x_seen += __popc(m);
-                while (m) {
-                    const int x = (w << 5) + __ffs(m) - 1;
-                    m &= m - 1u;
-                    const uint32_t *rx = rows + x * RS;
-                    unsigned c = __popc(cm[0] & rx[0]);
-                    if (W > 1) c += __popc(cm[1] & rx[1]);
-                    if (W > 2) c += __popc(cm[2] & rx[2]);
-                    if (W > 3) c += __popc(cm[3] & rx[3]);
-                    a32 += c;
+                for (int w = 0; w < 4; ++w) {
+                    uint32_t m = cm[w];
+                    x_seen += __popc(m);
+                    while (m) {
+                        const int x = (w << 5) + __ffs(m) - 1;
+                        m &= m - 1u;
+                        const uint4 r = *reinterpret_cast<const uint4 *>(rows + x * 4);
+                        a32 += __popc(cm[0] & r.x) + __popc(cm[1] & r.y) + __popc(cm[2] & r.z) +
+                               __popc(cm[3] & r.w);
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int w = 0; w < 4; ++w) {
+                    uint32_t m = cm[w];
+                    x_seen += __popc(m);
+                    while (m) {
+                        const int x = (w << 5) + __ffs(m) - 1;
+                        m &= m - 1u;
+                        const uint32_t *rx = rows + x * RS;
+                        unsigned c = __popc(cm[0] & rx[0]);
+                        if (W > 1) c += __popc(cm[1] & rx[1]);
+                        if (W > 2) c += __popc(cm[2] & rx[2]);
+                        if (W > 3) c += __popc(cm[3] & rx[3]);
+                        a32 += c;
+                    }
                 }
             }
             a += a32;
