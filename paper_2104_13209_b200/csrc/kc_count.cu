@@ -411,6 +411,7 @@ __global__ void __launch_bounds__(BLOCK) k_count(CountParams p) {
     sink.g_hist = p.hist;
     sink.L = p.hist_dim;
     sink.gq = (GQ && MODE == MODE_PIVOT) ? &p.gq : nullptr;  // compile-time off when !GQ
+    sink.eager = true;  // CTA tier
     sink.l2g = l2g;
     sink.hc = s_hc + 2 * warp;
     if ((tid & 31) == 0) {
@@ -596,6 +597,7 @@ __global__ void __launch_bounds__(BLOCK) k_count_warp(CountParams p) {
     sink.g_hist = p.hist;
     sink.L = p.hist_dim;
     sink.gq = (GQ && MODE == MODE_PIVOT) ? &p.gq : nullptr;  // compile-time off when !GQ
+    sink.eager = false;
     sink.l2g = l2g;
     sink.hc = s_hc + 2 * warp;
     for (int i = lane; i < hist_cells; i += 32) whist[i] = 0;

@@ -488,6 +488,7 @@ struct PivotLeafSink {
     int L;
     // GPU-wide work sharing (nullptr: off)
     const GQueue *gq;
+    bool eager;          // CTA tier: push large children without rate limit
     const int32_t *l2g;  // local id -> global vertex id of the current universe
     int *hc;             // per-warp smem: [0] countdown [1] cached hungry
     // uniform: should a child of n members be handed to a hungry warp?
@@ -495,15 +496,21 @@ struct PivotLeafSink {
     // donor keeps doing its own work and thieves get substantial subtrees.
     __device__ __forceinline__ bool want_push(int n, int room, int lane) const {
         if (!gq || n < kPushMin || n > kGItemMax) return false;
-        if (room < kPushRoom) return false;  // shallow remaining tree: cheaper to walk
+        if (eager) {
+            // CTA tier: hand every large (L-tier) child to a hungry warp-tier
+            // warp -- its W <= 4 universe walks it far cheaper than this one
+            if (n <= 32) return false;
+        } else if (room < kPushRoom) {
+            return false;  // shallow remaining tree: cheaper to walk
+        }
         if (lane == 0 && --hc[0] <= 0) {
-            hc[0] = kPushCooldown;
+            hc[0] = eager ? 16 : kPushCooldown;
             hc[1] = gq->vol(2);
         }
         __syncwarp();
         const bool w = hc[1] > 0;
         __syncwarp();
-        if (w && lane == 0) hc[1] = 0;  // one hand-over per cooldown window
+        if (w && lane == 0 && !eager) hc[1] = 0;  // one hand-over per cooldown window
         return w;
     }
     // reserve a slot (lock held by lane 0 on success); -1 when full / nobody hungry
@@ -1016,8 +1023,10 @@ __device__ void pivot_from(const uint32_t *__restrict__ rows, int RS, int W, int
                 const int nx = warp_count<WPL>(X);
                 if (WPL == 1 && sink.want_push(nx, allk ? 1 << 20 : t - s0, lane)) {
                     // donate the shallowest pending branch if there is one
-                    // below this frame, else this child
-                    if (s > s0) {
+                    // below this frame, else this child (CTA tier: this child)
+                    if (sink.eager) {
+                        if (push_large<WPL>(sink, X, list, s + 1, np2, lane)) continue;
+                    } else if (s > s0) {
                         if (lane == 0) F.at(s)[SC + 2] = uint32_t(v);  // cursor of the top frame
                         __syncwarp();
                         donate_bottom_L<WPL>(rows, RS, W, t, allk, F, s0, s, list, sink, lane,
