@@ -210,6 +210,11 @@ __global__ void k_peel_coop(const int64_t *__restrict__ row_ptr, const int32_t *
             level = mnv;  // no live vertex at this level: jump to the next one
             continue;
         }
+        // lower bound of the next level: min degree of the live vertices this
+        // scan left, lowered by every decrement of the rounds below; if it
+        // undershoots (its vertex got peeled), the next scan finds nothing and
+        // falls back to the exact minimum -- rounds and ranks are unchanged
+        int32_t next_level = mnv;
         int64_t end = tail + added;
         tail = end;
         degen = level > degen ? level : degen;
@@ -228,16 +233,20 @@ __global__ void k_peel_coop(const int64_t *__restrict__ row_ptr, const int32_t *
                     if (round_of[w] >= 0) continue;
                     const int32_t old = atomicSub(&deg[w], 1);
                     if (old == level + 1) order[tail + atomicAdd(&cnt[p % 3], 1)] = w;
+                    else if (old - 1 > level) atomicMin(&mn[p % 3], old - 1);
                 }
             }
             grid.sync();
             const int32_t nxt = vctl[p % 3];
+            const int32_t rmin = vctl[3 + p % 3];
+            next_level = rmin < next_level ? rmin : next_level;
             ++p;
             head = end;
             end = tail + nxt;
             tail = end;
             ++round;
         }
+        level = next_level;  // skip the scan that would only find this minimum
     }
     if (gtid == 0) {
         ctl[6] = degen;
