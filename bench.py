@@ -341,7 +341,8 @@ def run_ours(a):
             "metric": METRIC, "value": value, "unit": "k-cliques/s", "n_gpus": world,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": total_ms / a.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "u32 bitmaps / u64 counts (integer)", "data": "synthetic (seeded generator)",
+            "dtype": "u32", "dtype_note": "u32 bitmap words (AND/POPC), u64 count limbs",
+            "data": "synthetic (seeded generator)",
             "config": config_dict(a, world), "count": str(count),
             "phases_ms": {k: float(np.median(v)) for k, v in phase.items()},
             "d_max": rep.d_max, "degeneracy": rep.degeneracy, "visits": rep.load.total,
@@ -505,7 +506,7 @@ def run_reference(a):
         "impl": "reference", "metric": METRIC, "value": value, "unit": "k-cliques/s",
         "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
         "ms_per_step": float(np.mean(ms)), "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "u64 bitmaps / u128 counts (integer)",
+        "vs_baseline": None, "dtype": "u64",
         "data": "synthetic (seeded generator)", "config": config_dict(a, world),
         "cpu_baseline": cpu,
         "e2e": {"value": value, "unit": "k-cliques/s", "h2d_bytes_per_step": 0,
