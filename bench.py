@@ -409,7 +409,41 @@ def other_configs(kc, time_steps, local):
             out[name] = {"error": str(exc)[:200]}
     for _, gg in graphs.values():
         gg.free()
+    try:
+        out["ingest_rmat20_raw"] = ingest_side(kc, local)
+    except Exception as exc:
+        out["ingest_rmat20_raw"] = {"error": str(exc)[:200]}
     return out
+
+
+def ingest_side(kc, local):
+    """K0: the edge-list normal form of graph.py:93-109
+    on the raw RMAT-20 draws (16.8M pairs with loops and repeats), GPU vs the C
+    restatement (single-thread qsort), results compared element-wise."""
+    import oracle
+    from paper_2104_13209_b200 import synth
+
+    raw = synth.rmat_raw(20, 16, seed=1)
+    kc.normalize_edges(raw[:1024], device=local)  # warm-up (pool, module load)
+    dev_ms, wall_ms = [], []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        el, ms = kc.normalize_edges(raw, device=local, return_ms=True)
+        wall_ms.append((time.perf_counter() - t0) * 1e3)
+        dev_ms.append(ms)
+    t0 = time.perf_counter()
+    o_pairs, o_loops, o_self, o_dup = oracle.normalize_edges(raw)
+    cpu_ms = (time.perf_counter() - t0) * 1e3
+    match = (np.array_equal(el.edges, o_pairs) and np.array_equal(el.loop_ids, o_loops)
+             and (el.n_self_loops, el.n_duplicates) == (o_self, o_dup))
+    m_raw = raw.shape[0]
+    dev = float(np.median(dev_ms))
+    return {"m_raw": m_raw, "m_out": len(el), "n_self_loops": el.n_self_loops,
+            "n_duplicates": el.n_duplicates,
+            "gpu_ms": dev, "gpu_wall_ms": float(np.median(wall_ms)),
+            "gpu_note": "device events around H2D (pageable) + sort/unique + D2H",
+            "raw_pairs_per_s": m_raw / (dev / 1e3), "cpu_oracle_ms": cpu_ms,
+            "cpu_note": "oracle/kc_oracle.c oc_normalize_edges, 1 thread", "oracle_match": match}
 
 
 def roofline(kc, g, cfg, rep, a, local):

@@ -7,6 +7,7 @@
  * status codes.  Every device buffer is owned by the opaque kc_graph handle.
  *
  * Reference interfaces replaced (see INTEGRATION.md for the ctypes binding):
+ *   kc_normalize_edges    <- graph.py:93-109       load_edge_list's normal form (loops, dedup)
  *   kc_graph_from_edges   <- graph.py:162-200      from_edges(edges) -> Graph
  *   kc_graph_from_csr     <- graph.py:112-131      Graph(n, m, row_ptr, col, coo_src, orig_ids)
  *   kc_orient             <- orientation.py:116-153 compute_rank(g, criterion) + orient(g, ranking)
@@ -62,6 +63,17 @@ const char *kc_last_error(void);
 int kc_device_count(void);
 /* number of SMs of the device the graph lives on (load-stats width) */
 int kc_num_sms(int device);
+
+/* ---- edge-list normal form (graph.py:93-109) ------------------------ */
+/* raw: int64[2*m_raw] host pairs (row-major, ids >= 0, any order, loops and
+ * repeats allowed).  On the device: drop and tally self-loops (their ids,
+ * unique ascending, go to loop_ids_out), orient each pair (min, max), sort
+ * lexicographically, drop and tally repeats.  pairs_out: host int64[2*m_raw]
+ * capacity, receives m_out rows; loop_ids_out: host int64[m_raw] capacity.
+ * ms: device time (optional).  Negative ids -> KC_EINVAL. */
+int kc_normalize_edges(int device, const int64_t *raw, int64_t m_raw, int64_t *pairs_out,
+                       int64_t *m_out, int64_t *loop_ids_out, int64_t *n_loop_ids,
+                       int64_t *n_self_loops, int64_t *n_duplicates, double *ms);
 
 /* ---- graph construction (graph.py:162-200) ------------------------- */
 /* pairs: int64[2*m] host (any order; the reference normalizes beforehand),

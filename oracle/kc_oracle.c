@@ -109,6 +109,50 @@ static int cmp_u64(const void *a, const void *b) {
     return (x > y) - (x < y);
 }
 
+/* graph.py:93-109 (load_edge_list, after parsing): drop self-loops (tally them,
+ * keep their ids unique ascending), orient each pair (min, max), lexsort,
+ * drop repeats (tally them).  pairs_out: int64[2*m_raw]; loop_ids: int64[m_raw];
+ * counts[4] = {m_out, n_loop_ids, n_self_loops, n_duplicates}. */
+static int cmp_pair(const void *a, const void *b) {
+    const int64_t *x = (const int64_t *)a, *y = (const int64_t *)b;
+    if (x[0] != y[0]) return x[0] < y[0] ? -1 : 1;
+    return (x[1] > y[1]) - (x[1] < y[1]);
+}
+
+int oc_normalize_edges(const int64_t *raw, int64_t m_raw, int64_t *pairs_out, int64_t *loop_ids,
+                       int64_t *counts) {
+    int64_t n_self = 0, n_rest = 0;
+    for (int64_t i = 0; i < m_raw; ++i) {
+        int64_t u = raw[2 * i], v = raw[2 * i + 1];
+        if (u == v) { /* loops = u == v; loop_ids = unique(u[loops])   :96-98 */
+            loop_ids[n_self++] = u;
+            continue;
+        }
+        pairs_out[2 * n_rest] = u < v ? u : v; /* lo = minimum, hi = maximum :99-100 */
+        pairs_out[2 * n_rest + 1] = u < v ? v : u;
+        ++n_rest;
+    }
+    qsort(loop_ids, (size_t)n_self, sizeof(int64_t), cmp_i64);
+    int64_t n_loop_u = 0;
+    for (int64_t i = 0; i < n_self; ++i)
+        if (i == 0 || loop_ids[i] != loop_ids[i - 1]) loop_ids[n_loop_u++] = loop_ids[i];
+    qsort(pairs_out, (size_t)n_rest, 2 * sizeof(int64_t), cmp_pair); /* lexsort :101-102 */
+    int64_t n_keep = 0;
+    for (int64_t i = 0; i < n_rest; ++i) { /* keep[1:] = differs from previous :103-105 */
+        if (i && pairs_out[2 * i] == pairs_out[2 * i - 2] &&
+            pairs_out[2 * i + 1] == pairs_out[2 * i - 1])
+            continue;
+        pairs_out[2 * n_keep] = pairs_out[2 * i];
+        pairs_out[2 * n_keep + 1] = pairs_out[2 * i + 1];
+        ++n_keep;
+    }
+    counts[0] = n_keep;
+    counts[1] = n_loop_u;
+    counts[2] = n_self;
+    counts[3] = n_rest - n_keep;
+    return 0;
+}
+
 /* graph.py:177-181: ids = union1d(pairs.ravel(), extra) (sorted unique).
  * ids_out must hold 2*m + n_extra entries. */
 int oc_compact_ids(const int64_t *pairs, int64_t m, const int64_t *extra, int64_t n_extra,

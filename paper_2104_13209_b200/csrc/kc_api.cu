@@ -131,6 +131,26 @@ int kc_graph_from_edges(int device, const int64_t *pairs, int64_t m, const int64
     });
 }
 
+int kc_normalize_edges(int device, const int64_t *raw, int64_t m_raw, int64_t *pairs_out,
+                       int64_t *m_out, int64_t *loop_ids_out, int64_t *n_loop_ids,
+                       int64_t *n_self_loops, int64_t *n_duplicates, double *ms) {
+    return guarded([&] {
+        KC_REQUIRE(m_raw >= 0, KC_EINVAL, "negative size");
+        KC_REQUIRE(m_raw == 0 || (raw && pairs_out && loop_ids_out), KC_EINVAL,
+                   "NULL buffer");
+        kc_graph *g = new_graph(device);  // stream + scratch only; no graph is built
+        try {
+            kc_device_guard guard(device);
+            kc_do_normalize(g, raw, m_raw, pairs_out, m_out, loop_ids_out, n_loop_ids,
+                            n_self_loops, n_duplicates, ms);
+        } catch (...) {
+            destroy(g);
+            throw;
+        }
+        destroy(g);
+    });
+}
+
 int kc_graph_from_csr(int device, int64_t n, int64_t m, const int64_t *row_ptr, const int32_t *col,
                       const int64_t *orig_ids, kc_graph **out) {
     return guarded([&] {

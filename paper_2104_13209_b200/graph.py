@@ -1,7 +1,8 @@
 """Edge-list input and the device-resident CSR+COO graph.
 
 Mirrors the reference's ``graph`` module (graph.py): ``EdgeList``,
-``ParseError``, ``load_edge_list``, ``Graph``, ``from_edges``, ``read_graph``.
+``ParseError``, ``load_edge_list``, ``Graph``, ``from_edges``, ``read_graph``,
+plus ``normalize_edges`` (the edge-list normal form on the GPU).
 ``from_edges`` builds the CSR on the GPU (K1, csrc/kc_graph.cu); the host
 arrays of ``Graph`` are copied back lazily on first access, so the counting
 path never round-trips through host memory.
@@ -65,11 +66,9 @@ def _strict_parse(data: bytes) -> np.ndarray:
     return np.array(out, dtype=np.int64).reshape(-1, 2)
 
 
-def load_edge_list(text) -> EdgeList:
-    """Parse ``u v`` lines (``#`` comments) into a normalized EdgeList.
-
-    Self-loops and repeated pairs (either orientation) are dropped and counted.
-    """
+def parse_edge_pairs(text) -> np.ndarray:
+    """Parse ``u v`` lines (``#`` comments) into raw (m, 2) int64 pairs, in file
+    order, loops and repeats kept (the parsing half of graph.py:67-91)."""
     data = text.read() if hasattr(text, "read") else text
     if isinstance(data, str):
         data = data.encode()
@@ -84,9 +83,19 @@ def load_edge_list(text) -> EdgeList:
         arr = None
     if arr is None:
         arr = _strict_parse(data)
+    return np.ascontiguousarray(arr.reshape(-1, 2), dtype=np.int64)
+
+
+def load_edge_list(text) -> EdgeList:
+    """Parse ``u v`` lines (``#`` comments) into a normalized EdgeList.
+
+    Self-loops and repeated pairs (either orientation) are dropped and counted.
+    Host-side parse helper with the reference's exact semantics; the device
+    path for large inputs is ``normalize_edges`` (used by ``read_graph``).
+    """
+    arr = parse_edge_pairs(text)
     if arr.size == 0:
         return EdgeList(np.empty((0, 2), dtype=np.int64))
-    arr = arr.reshape(-1, 2)
     loops = arr[:, 0] == arr[:, 1]
     n_loops = int(loops.sum())
     loop_ids = np.unique(arr[loops, 0]) if n_loops else np.empty(0, dtype=np.int64)
@@ -95,6 +104,29 @@ def load_edge_list(text) -> EdgeList:
         return EdgeList(np.empty((0, 2), dtype=np.int64), n_loops, 0, loop_ids)
     uniq = np.unique(rest, axis=0)
     return EdgeList(uniq, n_loops, rest.shape[0] - uniq.shape[0], loop_ids)
+
+
+def normalize_edges(raw, device: int | None = None, return_ms: bool = False):
+    """Edge-list normal form on the GPU (K0, csrc/kc_ingest.cu).
+
+    Same result as the normalization half of ``load_edge_list``
+    (graph.py:93-109): self-loops dropped and tallied (ids kept as
+    ``loop_ids``), pairs oriented u < v, sorted, repeats dropped and tallied.
+    Negative ids raise ``ValueError``.
+    """
+    raw = np.ascontiguousarray(np.asarray(raw, dtype=np.int64).reshape(-1, 2))
+    m_raw = raw.shape[0]
+    pairs = np.empty((max(m_raw, 1), 2), dtype=np.int64)
+    loop_ids = np.empty(max(m_raw, 1), dtype=np.int64)
+    m_out, n_loop, n_self, n_dup = (ctypes.c_int64() for _ in range(4))
+    ms = ctypes.c_double()
+    dev = _lib.current_device() if device is None else device
+    _lib.check(_lib.load().kc_normalize_edges(
+        dev, _lib._ptr(raw), m_raw, _lib._ptr(pairs), ctypes.byref(m_out), _lib._ptr(loop_ids),
+        ctypes.byref(n_loop), ctypes.byref(n_self), ctypes.byref(n_dup), ctypes.byref(ms)))
+    el = EdgeList(pairs[:m_out.value].copy(), n_self.value, n_dup.value,
+                  loop_ids[:n_loop.value].copy())
+    return (el, float(ms.value)) if return_ms else el
 
 
 class Graph:
@@ -225,4 +257,4 @@ def read_graph(path, device: int | None = None) -> Graph:
         raw = f.read()
     if raw[:2] == b"\x1f\x8b":
         raw = gzip.decompress(raw)
-    return from_edges(load_edge_list(raw), device=device)
+    return from_edges(normalize_edges(parse_edge_pairs(raw), device=device), device=device)

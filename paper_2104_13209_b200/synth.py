@@ -48,6 +48,13 @@ def rmat(scale: int, edgefactor: int = 16, a=0.57, b=0.19, c=0.19, seed: int = 1
     permuted (as Graph500 does) so id order carries no degree information.
     Self-loops and duplicates are removed by ``normalize``.
     """
+    return normalize(rmat_raw(scale, edgefactor, a, b, c, seed, permute))
+
+
+def rmat_raw(scale: int, edgefactor: int = 16, a=0.57, b=0.19, c=0.19, seed: int = 1,
+             permute: bool = True) -> np.ndarray:
+    """The raw (m, 2) R-MAT draws of ``rmat`` in draw order, with their
+    self-loops and repeated pairs (an un-normalized edge list)."""
     rng = np.random.default_rng(seed)
     n = 1 << scale
     m = edgefactor * n
@@ -72,7 +79,7 @@ def rmat(scale: int, edgefactor: int = 16, a=0.57, b=0.19, c=0.19, seed: int = 1
         perm = rng.permutation(n).astype(np.int64)
         src = perm[src]
         dst = perm[dst]
-    return normalize(np.stack([src, dst], axis=1))
+    return np.stack([src, dst], axis=1)
 
 
 def planted_cliques(n: int = 50_000, n_cliques: int = 100, size_lo: int = 30,

@@ -225,8 +225,36 @@ def medium_suite(kc):
     return out
 
 
+def normalize_suite(kc):
+    """Reference load_edge_list (graph.py:67-109) on raw edge-list texts with
+    loops, repeats in both orders, comments and blank lines."""
+    rng = np.random.default_rng(93)
+    texts = ["", "# only a comment\n", "7 7\n", "3 1\n1 3\n2 2\n5 0\n2 2\n7 7\n",
+             "1 2\n\n# c\n2 1 # tail\n1 2\n"]
+    for trial in range(10):
+        hi = (40, 300, 5000, 1 << 40)[trial % 4]
+        m = int(rng.integers(1, 400))
+        raw = rng.integers(0, hi, size=(m, 2))
+        loops = rng.random(m) < 0.1
+        raw[loops, 1] = raw[loops, 0]
+        dup = rng.integers(0, m, size=m // 4)
+        raw = np.concatenate([raw, raw[dup][:, ::-1]])
+        texts.append("".join(f"{a} {b}\n" for a, b in raw.tolist()))
+    out = []
+    for i, text in enumerate(texts):
+        el = kc.load_edge_list(text)
+        out.append({"name": f"norm{i}", "text": text, "edges": el.edges.tolist(),
+                    "n_self_loops": el.n_self_loops, "n_duplicates": el.n_duplicates,
+                    "loop_ids": el.loop_ids.tolist()})
+    return out
+
+
 def main():
     kc = import_reference()
+    with open(os.path.join(HERE, "normalize.json"), "w") as f:
+        json.dump(normalize_suite(kc), f)
+    if "--normalize-only" in sys.argv:
+        return
     with open(os.path.join(HERE, "small.json"), "w") as f:
         json.dump(small_suite(kc), f)
     with open(os.path.join(HERE, "extract.json"), "w") as f:
