@@ -436,6 +436,13 @@ def ingest_side(kc, local):
     cpu_ms = (time.perf_counter() - t0) * 1e3
     match = (np.array_equal(el.edges, o_pairs) and np.array_equal(el.loop_ids, o_loops)
              and (el.n_self_loops, el.n_duplicates) == (o_self, o_dup))
+    fused = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        g = kc.from_raw_edges(raw, device=local)
+        fused.append(((time.perf_counter() - t0) * 1e3, g.normalize_ms, g.build_ms))
+        fused_nm = (g.n, g.m)
+        g.free()
     m_raw = raw.shape[0]
     dev = float(np.median(dev_ms))
     return {"m_raw": m_raw, "m_out": len(el), "n_self_loops": el.n_self_loops,
@@ -443,7 +450,12 @@ def ingest_side(kc, local):
             "gpu_ms": dev, "gpu_wall_ms": float(np.median(wall_ms)),
             "gpu_note": "device events around H2D (pageable) + sort/unique + D2H",
             "raw_pairs_per_s": m_raw / (dev / 1e3), "cpu_oracle_ms": cpu_ms,
-            "cpu_note": "oracle/kc_oracle.c oc_normalize_edges, 1 thread", "oracle_match": match}
+            "cpu_note": "oracle/kc_oracle.c oc_normalize_edges, 1 thread", "oracle_match": match,
+            "raw_to_csr": {"n": fused_nm[0], "m": fused_nm[1],
+                           "wall_ms": float(np.median([f[0] for f in fused])),
+                           "normalize_ms": float(np.median([f[1] for f in fused])),
+                           "csr_build_ms": float(np.median([f[2] for f in fused])),
+                           "note": "from_raw_edges: K0 kept on the device, then K1 (one H2D)"}}
 
 
 def roofline(kc, g, cfg, rep, a, local):

@@ -9,6 +9,7 @@
  * Reference interfaces replaced (see INTEGRATION.md for the ctypes binding):
  *   kc_normalize_edges    <- graph.py:93-109       load_edge_list's normal form (loops, dedup)
  *   kc_graph_from_edges   <- graph.py:162-200      from_edges(edges) -> Graph
+ *   kc_graph_from_raw_edges <- graph.py:203-209    read_graph: from_edges(load_edge_list(..)) after parsing
  *   kc_graph_from_csr     <- graph.py:112-131      Graph(n, m, row_ptr, col, coo_src, orig_ids)
  *   kc_orient             <- orientation.py:116-153 compute_rank(g, criterion) + orient(g, ranking)
  *   kc_count              <- scheduler.py:141-185  _worker_loop / _worker_loop_all + the
@@ -82,6 +83,13 @@ int kc_normalize_edges(int device, const int64_t *raw, int64_t m_raw, int64_t *p
  * sorts (src,dst), builds row_ptr on `device`. */
 int kc_graph_from_edges(int device, const int64_t *pairs, int64_t m, const int64_t *extra,
                         int64_t n_extra, kc_graph **out);
+/* read_graph's device path (graph.py:203-209 minus the text parse): K0's
+ * normal form of raw host pairs (see kc_normalize_edges), kept on the device
+ * and fed straight into the CSR build -- one H2D of the raw pairs, no round
+ * trip.  Loop-only ids become isolated vertices, as in from_edges(EdgeList).
+ * n_self_loops / n_duplicates / normalize_ms are optional outputs. */
+int kc_graph_from_raw_edges(int device, const int64_t *raw, int64_t m_raw, int64_t *n_self_loops,
+                            int64_t *n_duplicates, double *normalize_ms, kc_graph **out);
 /* upload an existing host CSR (Graph arrays); coo_src is derived */
 int kc_graph_from_csr(int device, int64_t n, int64_t m, const int64_t *row_ptr,
                       const int32_t *col, const int64_t *orig_ids, kc_graph **out);

@@ -23,7 +23,7 @@ SCHEME = {"vertex": 0, "edge": 1}
 # every symbol include/kclique.h declares (checked by tests/test_abi.py)
 EXPORTS = (
     "kc_abi_version", "kc_last_error", "kc_device_count", "kc_num_sms",
-    "kc_normalize_edges", "kc_graph_from_edges", "kc_graph_from_csr", "kc_graph_info", "kc_graph_download",
+    "kc_normalize_edges", "kc_graph_from_raw_edges", "kc_graph_from_edges", "kc_graph_from_csr", "kc_graph_info", "kc_graph_download",
     "kc_graph_free", "kc_graph_stream", "kc_orient", "kc_dag_download", "kc_count", "kc_num_tasks",
     "kc_task_costs", "kc_extract", "kc_count_bitgraph", "kc_find_pivot", "kc_probe",
 )
@@ -82,6 +82,10 @@ def load(path: str = LIB_PATH):
                                               _P, ctypes.POINTER(_i64), ctypes.POINTER(_i64),
                                               ctypes.POINTER(_i64),
                                               ctypes.POINTER(ctypes.c_double)]),
+        "kc_graph_from_raw_edges": (ctypes.c_int, [ctypes.c_int, _P, _i64, ctypes.POINTER(_i64),
+                                                   ctypes.POINTER(_i64),
+                                                   ctypes.POINTER(ctypes.c_double),
+                                                   ctypes.POINTER(_P)]),
         "kc_graph_from_edges": (ctypes.c_int, [ctypes.c_int, _P, _i64, _P, _i64,
                                                ctypes.POINTER(_P)]),
         "kc_graph_from_csr": (ctypes.c_int, [ctypes.c_int, _i64, _i64, _P, _P, _P,

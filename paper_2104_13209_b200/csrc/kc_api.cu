@@ -151,6 +151,32 @@ int kc_normalize_edges(int device, const int64_t *raw, int64_t m_raw, int64_t *p
     });
 }
 
+int kc_graph_from_raw_edges(int device, const int64_t *raw, int64_t m_raw, int64_t *n_self_loops,
+                            int64_t *n_duplicates, double *normalize_ms, kc_graph **out) {
+    return guarded([&] {
+        KC_REQUIRE(out, KC_EINVAL, "out is NULL");
+        KC_REQUIRE(m_raw >= 0 && (m_raw == 0 || raw), KC_EINVAL, "bad raw pairs");
+        *out = nullptr;
+        kc_graph *g = new_graph(device);
+        int64_t *d_pairs = nullptr, *d_loops = nullptr;
+        try {
+            kc_device_guard guard(device);
+            int64_t m = 0, n_loop = 0;
+            kc_do_normalize(g, raw, m_raw, nullptr, &m, nullptr, &n_loop, n_self_loops,
+                            n_duplicates, normalize_ms, &d_pairs, &d_loops);
+            kc_build_from_edges(g, d_pairs, m, d_loops, n_loop);
+            kc_free(d_pairs, g->stream);
+            kc_free(d_loops, g->stream);
+        } catch (...) {
+            kc_free(d_pairs, g->stream);
+            kc_free(d_loops, g->stream);
+            destroy(g);
+            throw;
+        }
+        *out = g;
+    });
+}
+
 int kc_graph_from_csr(int device, int64_t n, int64_t m, const int64_t *row_ptr, const int32_t *col,
                       const int64_t *orig_ids, kc_graph **out) {
     return guarded([&] {

@@ -421,9 +421,9 @@ void kc_build_from_edges(kc_graph *g, const int64_t *pairs, int64_t m, const int
     // ids = union1d(pairs.ravel(), extra)          graph.py:177-181
     int64_t *d_all = kc_alloc<int64_t>(tot, g->stream);
     int64_t *d_sorted = kc_alloc<int64_t>(tot, g->stream);
-    if (m) KC_CUDA(cudaMemcpyAsync(d_all, pairs, 16 * m, cudaMemcpyHostToDevice, g->stream));
+    if (m) KC_CUDA(cudaMemcpyAsync(d_all, pairs, 16 * m, cudaMemcpyDefault, g->stream));
     if (n_extra)
-        KC_CUDA(cudaMemcpyAsync(d_all + 2 * m, extra, 8 * n_extra, cudaMemcpyHostToDevice,
+        KC_CUDA(cudaMemcpyAsync(d_all + 2 * m, extra, 8 * n_extra, cudaMemcpyDefault,
                                 g->stream));
     int64_t n = 0;
     if (tot > 0) {
@@ -462,7 +462,7 @@ void kc_build_from_edges(kc_graph *g, const int64_t *pairs, int64_t m, const int
     } else {
         // raw pairs again (d_all now holds the ids); reuse a fresh buffer
         int64_t *d_pairs = kc_alloc<int64_t>(2 * m, g->stream);
-        KC_CUDA(cudaMemcpyAsync(d_pairs, pairs, 16 * m, cudaMemcpyHostToDevice, g->stream));
+        KC_CUDA(cudaMemcpyAsync(d_pairs, pairs, 16 * m, cudaMemcpyDefault, g->stream));
         int bits = kc_bits_for(n - 1 > 0 ? n - 1 : 1);
         KC_REQUIRE(2 * bits <= 64 && n < (int64_t(1) << 31), KC_EINVAL, "too many vertices");
         uint64_t *keys = kc_alloc<uint64_t>(2 * m, g->stream);

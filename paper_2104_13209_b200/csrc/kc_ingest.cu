@@ -120,7 +120,13 @@ int64_t read_count(const T *d, cudaStream_t s) {
 
 void kc_do_normalize(kc_graph *g, const int64_t *raw, int64_t m_raw, int64_t *pairs_out,
                      int64_t *m_out, int64_t *loop_ids_out, int64_t *n_loop_ids,
-                     int64_t *n_self_loops, int64_t *n_duplicates, double *ms) {
+                     int64_t *n_self_loops, int64_t *n_duplicates, double *ms,
+                     int64_t **dev_pairs, int64_t **dev_loop_ids) {
+    // dev_pairs / dev_loop_ids (optional): keep the results on the device and
+    // hand the buffers to the caller (stream-ordered on g->stream; the caller
+    // frees them) instead of copying them to pairs_out / loop_ids_out
+    if (dev_pairs) *dev_pairs = nullptr;
+    if (dev_loop_ids) *dev_loop_ids = nullptr;
     KC_REQUIRE(m_raw >= 0, KC_EINVAL, "negative size");
     KC_REQUIRE(m_raw < (int64_t(1) << 31), KC_EINVAL, "edge list too large");
     cudaStream_t s = g->stream;
@@ -232,18 +238,20 @@ void kc_do_normalize(kc_graph *g, const int64_t *raw, int64_t m_raw, int64_t *pa
                                               int(n_loops), s));
             n_loop_u = read_count(d_cnt + 1, s);
         }
-        if (pairs_out && n_keep)
+        if (pairs_out && n_keep && !dev_pairs)
             KC_CUDA(cudaMemcpyAsync(pairs_out, d_pairs, 16 * n_keep, cudaMemcpyDeviceToHost, s));
-        if (loop_ids_out && n_loop_u)
+        if (loop_ids_out && n_loop_u && !dev_loop_ids)
             KC_CUDA(cudaMemcpyAsync(loop_ids_out, loop_sel, 8 * n_loop_u, cudaMemcpyDeviceToHost,
                                     s));
         kc_free(d_raw, s);
         kc_free(d_max, s);
         kc_free(d_cnt, s);
         kc_free(loop_val, s);
-        kc_free(loop_sel, s);
         kc_free(loop_flag, s);
-        kc_free(d_pairs, s);
+        if (dev_loop_ids) *dev_loop_ids = loop_sel;
+        else kc_free(loop_sel, s);
+        if (dev_pairs) *dev_pairs = d_pairs;
+        else kc_free(d_pairs, s);
     }
     KC_CUDA(cudaEventRecord(e1, s));
     KC_CUDA(cudaEventSynchronize(e1));

@@ -106,9 +106,11 @@ static inline int kc_bits_for(int64_t x) {  // bits needed to hold 0..x
 // edge-list normal form (kc_ingest.cu)
 void kc_do_normalize(kc_graph *g, const int64_t *raw, int64_t m_raw, int64_t *pairs_out,
                      int64_t *m_out, int64_t *loop_ids_out, int64_t *n_loop_ids,
-                     int64_t *n_self_loops, int64_t *n_duplicates, double *ms);
+                     int64_t *n_self_loops, int64_t *n_duplicates, double *ms,
+                     int64_t **dev_pairs = nullptr, int64_t **dev_loop_ids = nullptr);
 
-// graph build / orientation (kc_graph.cu)
+// graph build / orientation (kc_graph.cu); pairs / extra may be host or
+// device pointers (copied with cudaMemcpyDefault)
 void kc_build_from_edges(kc_graph *g, const int64_t *pairs, int64_t m, const int64_t *extra,
                          int64_t n_extra);
 void kc_build_from_csr(kc_graph *g, int64_t n, int64_t m, const int64_t *row_ptr,

@@ -251,10 +251,26 @@ def from_edges(edges, device: int | None = None) -> Graph:
     return Graph(h, dev)
 
 
+def from_raw_edges(raw, device: int | None = None) -> Graph:
+    """``from_edges(load_edge_list(...))`` for already-parsed raw pairs, all on
+    the GPU: K0 normal form kept on the device, then K1.  The graph carries
+    ``n_self_loops``, ``n_duplicates`` and ``normalize_ms``."""
+    raw = np.ascontiguousarray(np.asarray(raw, dtype=np.int64).reshape(-1, 2))
+    dev = _lib.current_device() if device is None else device
+    h = ctypes.c_void_p()
+    n_self, n_dup, ms = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_double()
+    _lib.check(_lib.load().kc_graph_from_raw_edges(dev, _lib._ptr(raw), raw.shape[0],
+                                                   ctypes.byref(n_self), ctypes.byref(n_dup),
+                                                   ctypes.byref(ms), ctypes.byref(h)))
+    g = Graph(h, dev)
+    g.n_self_loops, g.n_duplicates, g.normalize_ms = n_self.value, n_dup.value, ms.value
+    return g
+
+
 def read_graph(path, device: int | None = None) -> Graph:
     """SNAP-style edge list (plain or gzip) -> device Graph (graph.py:203-209)."""
     with open(path, "rb") as f:
         raw = f.read()
     if raw[:2] == b"\x1f\x8b":
         raw = gzip.decompress(raw)
-    return from_edges(normalize_edges(parse_edge_pairs(raw), device=device), device=device)
+    return from_raw_edges(parse_edge_pairs(raw), device=device)
