@@ -43,10 +43,23 @@ struct pair_decomposer {
     }
 };
 
-// per raw row: loop flag + loop id, and the oriented key (sentinel for loops)
+// warp-aggregated append of the loop ids (loops are rare: no per-row stream)
+__device__ __forceinline__ void append_loop(bool loop, int64_t u, int64_t *__restrict__ loop_out,
+                                            unsigned long long *__restrict__ loop_cnt) {
+    const unsigned act = __activemask();
+    const unsigned bal = __ballot_sync(act, loop);
+    if (!bal) return;
+    const int lane = threadIdx.x & 31, leader = __ffs(bal) - 1;
+    unsigned long long base = 0;
+    if (lane == leader) base = atomicAdd(loop_cnt, (unsigned long long)__popc(bal));
+    base = __shfl_sync(act, base, leader);
+    if (loop) loop_out[base + __popc(bal & ((1u << lane) - 1))] = u;
+}
+
+// per raw row: the oriented key (sentinel for loops); loop ids appended
 __global__ void k_orient_pack(const int64_t *__restrict__ raw, int64_t m, int bits,
-                              uint64_t *__restrict__ keys, int64_t *__restrict__ loop_val,
-                              uint8_t *__restrict__ loop_flag) {
+                              uint64_t *__restrict__ keys, int64_t *__restrict__ loop_out,
+                              unsigned long long *__restrict__ loop_cnt) {
     const uint64_t sentinel = (bits >= 32) ? ~uint64_t(0) : ((uint64_t(1) << (2 * bits)) - 1);
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m;
          i += int64_t(gridDim.x) * blockDim.x) {
@@ -54,14 +67,13 @@ __global__ void k_orient_pack(const int64_t *__restrict__ raw, int64_t m, int bi
         const bool loop = u == v;
         const uint64_t lo = uint64_t(u < v ? u : v), hi = uint64_t(u < v ? v : u);
         keys[i] = loop ? sentinel : ((lo << bits) | hi);
-        loop_val[i] = u;
-        loop_flag[i] = loop;
+        append_loop(loop, u, loop_out, loop_cnt);
     }
 }
 
 __global__ void k_orient_wide(const int64_t *__restrict__ raw, int64_t m,
-                              pair_key *__restrict__ keys, int64_t *__restrict__ loop_val,
-                              uint8_t *__restrict__ loop_flag) {
+                              pair_key *__restrict__ keys, int64_t *__restrict__ loop_out,
+                              unsigned long long *__restrict__ loop_cnt) {
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m;
          i += int64_t(gridDim.x) * blockDim.x) {
         const int64_t u = raw[2 * i], v = raw[2 * i + 1];
@@ -70,8 +82,7 @@ __global__ void k_orient_wide(const int64_t *__restrict__ raw, int64_t m,
         k.lo = loop ? INT64_MAX : (u < v ? u : v);
         k.hi = loop ? INT64_MAX : (u < v ? v : u);
         keys[i] = k;
-        loop_val[i] = u;
-        loop_flag[i] = loop;
+        append_loop(loop, u, loop_out, loop_cnt);
     }
 }
 
@@ -153,7 +164,8 @@ void kc_do_normalize(kc_graph *g, const int64_t *raw, int64_t m_raw, int64_t *pa
         }
         int64_t *loop_val = kc_alloc<int64_t>(m_raw, s);
         int64_t *loop_sel = kc_alloc<int64_t>(m_raw, s);
-        uint8_t *loop_flag = kc_alloc<uint8_t>(m_raw, s);
+        unsigned long long *loop_cnt = kc_alloc<unsigned long long>(1, s);
+        KC_CUDA(cudaMemsetAsync(loop_cnt, 0, 8, s));
         int64_t *d_pairs = kc_alloc<int64_t>(2 * m_raw, s);
         size_t bytes = 0;
         // max_id + 1 must stay unused so the all-ones key is a free sentinel
@@ -163,7 +175,7 @@ void kc_do_normalize(kc_graph *g, const int64_t *raw, int64_t m_raw, int64_t *pa
             uint64_t *keys2 = kc_alloc<uint64_t>(m_raw, s);
             k_orient_pack<<<grid_for(m_raw, g->num_sms), kThreads, 0, s>>>(d_raw, m_raw, bits,
                                                                             keys, loop_val,
-                                                                            loop_flag);
+                                                                            loop_cnt);
             KC_CUDA(cudaGetLastError());
             // lexsort((hi, lo))                          graph.py:101-102
             KC_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, bytes, keys, keys2, int(m_raw), 0,
@@ -192,7 +204,7 @@ void kc_do_normalize(kc_graph *g, const int64_t *raw, int64_t m_raw, int64_t *pa
             pair_key *keys = kc_alloc<pair_key>(m_raw, s);
             pair_key *keys2 = kc_alloc<pair_key>(m_raw, s);
             k_orient_wide<<<grid_for(m_raw, g->num_sms), kThreads, 0, s>>>(d_raw, m_raw, keys,
-                                                                            loop_val, loop_flag);
+                                                                            loop_val, loop_cnt);
             KC_CUDA(cudaGetLastError());
             KC_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, bytes, keys, keys2, int(m_raw),
                                                    pair_decomposer{}, s));
@@ -215,41 +227,36 @@ void kc_do_normalize(kc_graph *g, const int64_t *raw, int64_t m_raw, int64_t *pa
             kc_free(keys, s);
             kc_free(keys2, s);
         }
-        // self-loop ids: compact, sort, unique          graph.py:97-98
-        bytes = 0;
-        KC_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, loop_val, loop_flag, loop_sel,
-                                           d_cnt + 1, int(m_raw), s));
-        void *tmp = kc_tmp(g, bytes);
-        KC_CUDA(cub::DeviceSelect::Flagged(tmp, bytes, loop_val, loop_flag, loop_sel, d_cnt + 1,
-                                           int(m_raw), s));
-        n_loops = read_count(d_cnt + 1, s);
+        // self-loop ids (appended by the pack kernel): sort, unique   graph.py:97-98
+        n_loops = read_count(loop_cnt, s);
+        void *tmp = nullptr;
         if (n_loops) {
             bytes = 0;
-            KC_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, bytes, loop_sel, loop_val,
+            KC_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, bytes, loop_val, loop_sel,
                                                    int(n_loops), 0, 64, s));
             tmp = kc_tmp(g, bytes);
-            KC_CUDA(cub::DeviceRadixSort::SortKeys(tmp, bytes, loop_sel, loop_val, int(n_loops),
+            KC_CUDA(cub::DeviceRadixSort::SortKeys(tmp, bytes, loop_val, loop_sel, int(n_loops),
                                                    0, 64, s));
             bytes = 0;
-            KC_CUDA(cub::DeviceSelect::Unique(nullptr, bytes, loop_val, loop_sel, d_cnt + 1,
+            KC_CUDA(cub::DeviceSelect::Unique(nullptr, bytes, loop_sel, loop_val, d_cnt + 1,
                                               int(n_loops), s));
             tmp = kc_tmp(g, bytes);
-            KC_CUDA(cub::DeviceSelect::Unique(tmp, bytes, loop_val, loop_sel, d_cnt + 1,
+            KC_CUDA(cub::DeviceSelect::Unique(tmp, bytes, loop_sel, loop_val, d_cnt + 1,
                                               int(n_loops), s));
             n_loop_u = read_count(d_cnt + 1, s);
         }
         if (pairs_out && n_keep && !dev_pairs)
             KC_CUDA(cudaMemcpyAsync(pairs_out, d_pairs, 16 * n_keep, cudaMemcpyDeviceToHost, s));
         if (loop_ids_out && n_loop_u && !dev_loop_ids)
-            KC_CUDA(cudaMemcpyAsync(loop_ids_out, loop_sel, 8 * n_loop_u, cudaMemcpyDeviceToHost,
+            KC_CUDA(cudaMemcpyAsync(loop_ids_out, loop_val, 8 * n_loop_u, cudaMemcpyDeviceToHost,
                                     s));
         kc_free(d_raw, s);
         kc_free(d_max, s);
         kc_free(d_cnt, s);
-        kc_free(loop_val, s);
-        kc_free(loop_flag, s);
-        if (dev_loop_ids) *dev_loop_ids = loop_sel;
-        else kc_free(loop_sel, s);
+        kc_free(loop_sel, s);
+        kc_free(loop_cnt, s);
+        if (dev_loop_ids) *dev_loop_ids = loop_val;
+        else kc_free(loop_val, s);
         if (dev_pairs) *dev_pairs = d_pairs;
         else kc_free(d_pairs, s);
     }
