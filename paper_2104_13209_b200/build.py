@@ -22,7 +22,7 @@ INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 LIB = os.path.join(HERE, "libkc.so")
 BUILD = os.path.join(HERE, "_build")
 SOURCES = ["kc_ingest.cu", "kc_graph.cu", "kc_count.cu", "kc_probe.cu", "kc_api.cu"]
-HEADERS = ["kc_internal.cuh"]
+HEADERS = ["kc_internal.cuh", "kc_traverse.cuh"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",

@@ -190,6 +190,40 @@ __device__ __forceinline__ int score_sum(const uint32_t *__restrict__ rows, int 
 // j-th member v of C and walks X_v itself (3-way AND + POPC per word), so the
 // per-visit ballot/shuffle work of the sequential walk disappears for the two
 // levels that hold almost all visits.  cbuf: per-warp copy of C (32*WPL words).
+// Harley-Seal carry-save popcount accumulator.  The last orientation level
+// sums popc(C & row x) over many words; instead of one POPC per word (the
+// XU pipe, 16 lanes/clk/SM -- the measured bound of the pair loops) the words
+// go through full adders (two LOP3 each, 64 lanes/clk/SM) into weight-1 and
+// weight-2 bit planes, and only the weight-4 carries are popcounted: one POPC
+// per four words.  The sum is exact: total = popc(ones) + 2 popc(twos) + 4 fours.
+struct CsaAcc {
+    uint32_t ones = 0, twos = 0;
+    unsigned fours = 0;
+    __device__ __forceinline__ static void fa(uint32_t &carry, uint32_t &sum, uint32_t a,
+                                              uint32_t b, uint32_t c) {
+        const uint32_t u = a ^ b;
+        carry = (a & b) | (u & c);
+        sum = u ^ c;
+    }
+    __device__ __forceinline__ void add4(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+        uint32_t ca, cb, c4;
+        fa(ca, ones, ones, a, b);
+        fa(cb, ones, ones, c, d);
+        fa(c4, twos, twos, ca, cb);
+        fours += unsigned(__popc(c4));
+    }
+    __device__ __forceinline__ void add2(uint32_t a, uint32_t b) {
+        uint32_t ca;
+        fa(ca, ones, ones, a, b);
+        const uint32_t c4 = twos & ca;
+        twos ^= ca;
+        fours += unsigned(__popc(c4));
+    }
+    __device__ __forceinline__ unsigned total() const {
+        return 4u * fours + unsigned(__popc(ones)) + 2u * unsigned(__popc(twos));
+    }
+};
+
 template <int WPL>
 __device__ __forceinline__ void score_pairs(const uint32_t *__restrict__ rows, int RS, int W,
                                             const Set<WPL> &C, int *list, uint32_t *cbuf,
@@ -221,18 +255,21 @@ __device__ __forceinline__ void score_pairs(const uint32_t *__restrict__ rows, i
             for (int w = 0; w < 4; ++w) cm[w] = w < W ? (cbuf[w] & rv[w]) : 0u;
             unsigned a32 = 0;
             if (RS == 4) {  // 16-byte rows (warp tier, orientation): one LDS.128 per member
+                // members in any order (the sum is order-free): top bit first
+                // needs one FLO, no BREV; words summed through CsaAcc
+                CsaAcc h;
 #pragma unroll
                 for (int w = 0; w < 4; ++w) {
                     uint32_t m = cm[w];
                     x_seen += __popc(m);
                     while (m) {
-                        const int x = (w << 5) + __ffs(m) - 1;
-                        m &= m - 1u;
-                        const uint4 r = *reinterpret_cast<const uint4 *>(rows + x * 4);
-                        a32 += __popc(cm[0] & r.x) + __popc(cm[1] & r.y) + __popc(cm[2] & r.z) +
-                               __popc(cm[3] & r.w);
+                        const int b = 31 - __clz(m);
+                        m ^= 1u << b;
+                        const uint4 r = *reinterpret_cast<const uint4 *>(rows + ((w << 5) + b) * 4);
+                        h.add4(cm[0] & r.x, cm[1] & r.y, cm[2] & r.z, cm[3] & r.w);
                     }
                 }
+                a32 = h.total();
             } else {
 #pragma unroll
                 for (int w = 0; w < 4; ++w) {
@@ -365,20 +402,22 @@ __device__ __forceinline__ void pairs_small(const uint32_t *srow, uint32_t C, in
         const int xs = __popc(m);
         visits += ull(1 + xs);
         work += ull(1 + xs);
-        // two members per trip: independent shared loads in flight, 32-bit sums
-        unsigned a0 = 0, a1 = 0;
+        // two members per trip: independent shared loads in flight; the
+        // words go through CsaAcc (one POPC per four members)
+        CsaAcc h;
         while (m) {
-            const int x0 = __ffs(m) - 1;
-            m &= m - 1u;
+            const int x0 = 31 - __clz(m);
+            m ^= 1u << x0;
             const uint32_t r0 = srow[x0];
+            uint32_t r1 = 0;
             if (m) {
-                const int x1 = __ffs(m) - 1;
-                m &= m - 1u;
-                a1 += __popc(cm & srow[x1]);
+                const int x1 = 31 - __clz(m);
+                m ^= 1u << x1;
+                r1 = srow[x1];
             }
-            a0 += __popc(cm & r0);
+            h.add2(cm & r0, cm & r1);
         }
-        acc += ull(a0 + a1);
+        acc += ull(h.total());
     }
 }
 
