@@ -445,8 +445,10 @@ __device__ void orient_small(const uint32_t *srow, uint32_t C, int s, int last, 
             R = __shfl_sync(FULL, fR, s - s0);
             continue;
         }
-        const int v = __ffs(R) - 1;
-        R &= R - 1u;
+        // orientation counts and visits do not depend on the branch order:
+        // take the top member (one FLO, no BREV)
+        const int v = 31 - __clz(R);
+        R ^= 1u << v;
         ++uvis;
         const uint32_t X = C & srow[v];
         if (!X) continue;
