@@ -428,27 +428,11 @@ void kc_build_from_edges(kc_graph *g, const int64_t *pairs, int64_t m, const int
     int64_t n = 0;
     if (tot > 0) {
         KC_REQUIRE(tot < (int64_t(1) << 31), KC_EINVAL, "edge list too large");
-        // radix passes only over the bits the ids use (ids >= 0 in practice;
-        // any negative id keeps the full signed 64-bit sort)
-        int64_t *d_mm = kc_alloc<int64_t>(2, g->stream);
         size_t bytes = 0;
-        KC_CUDA(cub::DeviceReduce::Min(nullptr, bytes, d_all, d_mm, int(tot), g->stream));
+        KC_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, bytes, d_all, d_sorted, int(tot), 0, 64,
+                                               g->stream));
         void *tmp = kc_tmp(g, bytes);
-        KC_CUDA(cub::DeviceReduce::Min(tmp, bytes, d_all, d_mm, int(tot), g->stream));
-        bytes = 0;
-        KC_CUDA(cub::DeviceReduce::Max(nullptr, bytes, d_all, d_mm + 1, int(tot), g->stream));
-        tmp = kc_tmp(g, bytes);
-        KC_CUDA(cub::DeviceReduce::Max(tmp, bytes, d_all, d_mm + 1, int(tot), g->stream));
-        int64_t mm[2] = {0, 0};
-        KC_CUDA(cudaMemcpyAsync(mm, d_mm, 16, cudaMemcpyDeviceToHost, g->stream));
-        KC_CUDA(cudaStreamSynchronize(g->stream));
-        kc_free(d_mm, g->stream);
-        const int id_bits = mm[0] < 0 ? 64 : kc_bits_for(mm[1]);
-        bytes = 0;
-        KC_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, bytes, d_all, d_sorted, int(tot), 0,
-                                               id_bits, g->stream));
-        tmp = kc_tmp(g, bytes);
-        KC_CUDA(cub::DeviceRadixSort::SortKeys(tmp, bytes, d_all, d_sorted, int(tot), 0, id_bits,
+        KC_CUDA(cub::DeviceRadixSort::SortKeys(tmp, bytes, d_all, d_sorted, int(tot), 0, 64,
                                                g->stream));
         int32_t *d_n = kc_alloc<int32_t>(1, g->stream);
         bytes = 0;
