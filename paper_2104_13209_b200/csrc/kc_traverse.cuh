@@ -293,32 +293,25 @@ __device__ __forceinline__ void score_pairs(const uint32_t *__restrict__ rows, i
             uint32_t nzm = 0;
             for (int w = 0; w < W; ++w) nzm |= (cbuf[w] & rv[w]) ? (1u << w) : 0u;
             uint32_t ws = nzm;
-            CsaAcc h;  // word order is irrelevant to the sum: top bits first
             while (ws) {
-                const int w = 31 - __clz(ws);
-                ws ^= 1u << w;
+                const int w = __ffs(ws) - 1;
+                ws &= ws - 1u;
                 uint32_t m = cbuf[w] & rv[w];
                 x_seen += __popc(m);
                 while (m) {
-                    const int b = 31 - __clz(m);
-                    m ^= 1u << b;
-                    const uint32_t *rx = rows + ((w << 5) + b) * RS;
+                    const int x = (w << 5) + __ffs(m) - 1;
+                    m &= m - 1u;
+                    const uint32_t *rx = rows + x * RS;
                     uint32_t w2s = nzm;
+                    int c = 0;
                     while (w2s) {
-                        const int w2 = 31 - __clz(w2s);
-                        w2s ^= 1u << w2;
-                        const uint32_t a0 = cbuf[w2] & rv[w2] & rx[w2];
-                        uint32_t a1 = 0;
-                        if (w2s) {
-                            const int w3 = 31 - __clz(w2s);
-                            w2s ^= 1u << w3;
-                            a1 = cbuf[w3] & rv[w3] & rx[w3];
-                        }
-                        h.add2(a0, a1);
+                        const int w2 = __ffs(w2s) - 1;
+                        w2s &= w2s - 1u;
+                        c += __popc(cbuf[w2] & rv[w2] & rx[w2]);
                     }
+                    a += c;
                 }
             }
-            a += h.total();
         } else {
             for (int w = 0; w < W; ++w) {
                 uint32_t m = cbuf[w] & rv[w];
