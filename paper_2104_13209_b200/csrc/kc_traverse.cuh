@@ -148,6 +148,48 @@ __device__ __forceinline__ int compact(const Set<WPL> &C, int *list, int lane) {
 
 // popc(C & row v) for this lane's v (valid) over the nonzero words of C.
 // All lanes must call it (shuffles); invalid lanes pass v = 0, valid = false.
+template <int WPL>
+__device__ __forceinline__ int cover(const uint32_t *__restrict__ rows, int RS,
+                                     const Set<WPL> &C, int v, bool valid) {
+    int cov = 0;
+    const uint32_t *rv = rows + v * RS;
+#pragma unroll
+    for (int p = 0; p < WPL; ++p) {
+        unsigned nz = __ballot_sync(FULL, C.w[p] != 0);
+        while (nz) {
+            const int L = __ffs(nz) - 1;
+            nz &= nz - 1u;
+            const uint32_t cw = __shfl_sync(FULL, C.w[p], L);
+            if (valid) cov += __popc(cw & rv[p * 32 + L]);
+        }
+    }
+    return cov;
+}
+
+// sum over v in C of popc(C & row v); the sum lands in the calling lanes'
+// accumulators (reduced at kernel end).  Returns |C| (uniform).
+template <int WPL>
+__device__ __forceinline__ int score_sum(const uint32_t *__restrict__ rows, int RS,
+                                         const Set<WPL> &C, int *list, int lane, ull &acc,
+                                         ull &work, int W) {
+    const int n = compact<WPL>(C, list, lane);
+    for (int base = 0; base < n; base += 32) {
+        const int i = base + lane;
+        const bool ok = i < n;
+        const int v = ok ? list[i] : 0;
+        acc += ull(cover<WPL>(rows, RS, C, v, ok));
+    }
+    if (lane == 0) work += ull(n);
+    __syncwarp();
+    return n;
+}
+
+// The last TWO orientation levels at once, lane-parallel over v in C
+// (frame last-1 = C): every v in C is a visit, each x in X_v = C & row v is a
+// visit of the last frame contributing popc(X_v & row x).  Lane j owns the
+// j-th member v of C and walks X_v itself (3-way AND + POPC per word), so the
+// per-visit ballot/shuffle work of the sequential walk disappears for the two
+// levels that hold almost all visits.  cbuf: per-warp copy of C (32*WPL words).
 // Harley-Seal carry-save popcount accumulator.  The last orientation level
 // sums popc(C & row x) over many words; instead of one POPC per word (the
 // XU pipe, 16 lanes/clk/SM -- the measured bound of the pair loops) the words
@@ -182,56 +224,6 @@ struct CsaAcc {
     }
 };
 
-template <int WPL>
-__device__ __forceinline__ int cover(const uint32_t *__restrict__ rows, int RS,
-                                     const Set<WPL> &C, int v, bool valid) {
-    // words in pairs through CsaAcc (the word loop is warp-uniform, so the
-    // pairing is too): one POPC per two nonzero words plus two at the end
-    CsaAcc h;
-    uint32_t pend = 0;
-    bool have = false;
-    const uint32_t *rv = rows + v * RS;
-#pragma unroll
-    for (int p = 0; p < WPL; ++p) {
-        unsigned nz = __ballot_sync(FULL, C.w[p] != 0);
-        while (nz) {
-            const int L = __ffs(nz) - 1;
-            nz &= nz - 1u;
-            const uint32_t cw = __shfl_sync(FULL, C.w[p], L);
-            const uint32_t x = valid ? (cw & rv[p * 32 + L]) : 0u;
-            if (have) h.add2(pend, x);
-            else pend = x;
-            have = !have;
-        }
-    }
-    if (have) return int(h.total()) + __popc(pend);
-    return int(h.total());
-}
-
-// sum over v in C of popc(C & row v); the sum lands in the calling lanes'
-// accumulators (reduced at kernel end).  Returns |C| (uniform).
-template <int WPL>
-__device__ __forceinline__ int score_sum(const uint32_t *__restrict__ rows, int RS,
-                                         const Set<WPL> &C, int *list, int lane, ull &acc,
-                                         ull &work, int W) {
-    const int n = compact<WPL>(C, list, lane);
-    for (int base = 0; base < n; base += 32) {
-        const int i = base + lane;
-        const bool ok = i < n;
-        const int v = ok ? list[i] : 0;
-        acc += ull(cover<WPL>(rows, RS, C, v, ok));
-    }
-    if (lane == 0) work += ull(n);
-    __syncwarp();
-    return n;
-}
-
-// The last TWO orientation levels at once, lane-parallel over v in C
-// (frame last-1 = C): every v in C is a visit, each x in X_v = C & row v is a
-// visit of the last frame contributing popc(X_v & row x).  Lane j owns the
-// j-th member v of C and walks X_v itself (3-way AND + POPC per word), so the
-// per-visit ballot/shuffle work of the sequential walk disappears for the two
-// levels that hold almost all visits.  cbuf: per-warp copy of C (32*WPL words).
 template <int WPL>
 __device__ __forceinline__ void score_pairs(const uint32_t *__restrict__ rows, int RS, int W,
                                             const Set<WPL> &C, int *list, uint32_t *cbuf,
