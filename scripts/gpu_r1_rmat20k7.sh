@@ -1,0 +1,6 @@
+#!/bin/bash
+mkdir -p gpurun_out
+export KC_GRAPH_CACHE=/tmp/kc_graphs
+export PYTHONPATH=$PWD
+timeout 600 python scripts/explore.py --workload rmat20 --k 7 --algo orient --scheme vertex --criterion degeneracy --reps 1 > gpurun_out/rmat20_k7.log 2>&1
+echo done
