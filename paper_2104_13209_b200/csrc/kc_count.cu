@@ -738,9 +738,19 @@ __global__ void __launch_bounds__(BLOCK) k_count_warp(CountParams p) {
                             q.release();
                         }
                     } else if (kc_globaltimer() - t_start > 20000000ull) {  // 20 ms idle
-                        // give the SM back; the lock orders this with pushers'
-                        // `hungry` check, so no item can be stranded
+                        // give the SM back.  Under the lock: an item a pusher
+                        // published since the poll above is taken, not left
+                        // behind; otherwise `hungry` drops before any later
+                        // pusher's check (reserve() re-reads it under the
+                        // lock), so no item can be stranded
                         q.acquire();
+                        const int sz2 = q.vol(1);
+                        if (sz2 > 0) {
+                            slot = sz2 - 1;  // lock kept while the item is copied out
+                            atomicSub(q.ctl + 2, 1);
+                            atomicAdd(q.ctl + 3, 1);
+                            break;
+                        }
                         atomicSub(q.ctl + 2, 1);
                         q.release();
                         done = 1;
@@ -1034,6 +1044,12 @@ int64_t build_tasks(kc_graph *g, int scheme, int64_t lo, int64_t hi, int min_d, 
 
 constexpr int kBlock = 128;
 constexpr int kSmidSlots = 1024;  // %smid can exceed the SM count
+// kc_do_count's counter block `outs` (u64 words): [0] task counter, [1..4]
+// limbs, [5] visits, [6] tasks run, [7] warp-tier counter, [8, 8+kSmidSlots)
+// visits per SM, then word_ops, extract bytes, four more task counters and
+// the overflow count, then the subtree queue's control words (8 ints)
+constexpr int kOutGq = 8 + kSmidSlots + 8;
+constexpr int kOutWords = kOutGq + 4;
 constexpr int kSmemMax = 220 * 1024;
 constexpr int kSmemTarget = 100 * 1024;  // aim for >= 2 resident CTAs per SM
 
@@ -1045,6 +1061,19 @@ int frames_needed(int mode, int t, int dcap) {
 }
 
 typedef std::vector<std::unique_ptr<DevBuf>> Keep;
+
+// DevBuf memory is stream-ordered on the graph stream; a kernel launched on
+// another stream (the aux stream of the concurrent warp tier) must not start
+// before those allocations -- the pool may hand it blocks the graph stream
+// freed a moment ago while its kernels still read them
+void order_after_allocs(kc_graph *g, cudaStream_t stream) {
+    if (stream == g->stream) return;
+    cudaEvent_t ev;
+    KC_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    KC_CUDA(cudaEventRecord(ev, g->stream));
+    KC_CUDA(cudaStreamWaitEvent(stream, ev, 0));
+    KC_CUDA(cudaEventDestroy(ev));
+}
 
 template <int MODE, int WPL>
 void launch_wpl(kc_graph *g, CountParams &p, int grid_override, Keep &keep,
@@ -1095,6 +1124,7 @@ void launch_wpl(kc_graph *g, CountParams &p, int grid_override, Keep &keep,
         keep.emplace_back(new DevBuf(4 * size_t(p.frames_slot) * size_t(grid) * NW));
         p.frames_global = keep.back()->as<uint32_t>();
     }
+    order_after_allocs(g, stream);
     kern<<<grid, kBlock, smem, stream>>>(p);
     KC_CUDA(cudaGetLastError());
 }
@@ -1127,6 +1157,7 @@ void launch_warp(kc_graph *g, CountParams &p, Keep &keep, cudaStream_t stream) {
         keep.emplace_back(new DevBuf(4 * size_t(p.frames_slot) * size_t(grid) * NW));
         p.frames_global = keep.back()->as<uint32_t>();
     }
+    order_after_allocs(g, stream);
     kern<<<grid, kBlock, smem, stream>>>(p);
     KC_CUDA(cudaGetLastError());
 }
@@ -1212,8 +1243,8 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
                               vsel.as<uint8_t>());
     }
 
-    DevBuf outs(8 * (20 + size_t(kSmidSlots)));
-    KC_CUDA(cudaMemsetAsync(outs.p, 0, 8 * (20 + size_t(kSmidSlots)), g->stream));
+    DevBuf outs(8 * size_t(kOutWords));
+    KC_CUDA(cudaMemsetAsync(outs.p, 0, 8 * size_t(kOutWords), g->stream));
     DevBuf dhist(pivot ? 8 * size_t(L * L) : 8);
     if (pivot) KC_CUDA(cudaMemsetAsync(dhist.p, 0, 8 * size_t(L * L), g->stream));
 
@@ -1248,10 +1279,11 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
     KC_CUDA(cudaEventCreateWithFlags(&e_fork, cudaEventDisableTiming));
     KC_CUDA(cudaEventCreateWithFlags(&e_join, cudaEventDisableTiming));
     KC_CUDA(cudaEventRecord(e0, g->stream));
-    DevBuf gq_items(pivot ? 4 * size_t(kGqCap) * kct::kGItemWords : 4), gq_ctl(32);
-    KC_CUDA(cudaMemsetAsync(gq_ctl.p, 0, 32, g->stream));
+    DevBuf gq_items(pivot ? 4 * size_t(kGqCap) * kct::kGItemWords : 4);
     p.gq.items = gq_items.as<uint32_t>();
-    p.gq.ctl = gq_ctl.as<int>();
+    // queue control words live in `outs` (zeroed above) so the final copy
+    // brings them back with the counters: the host checks the queue drained
+    p.gq.ctl = reinterpret_cast<int *>(o + kOutGq);
     p.gq.cap = kGqCap;
     // GPU-wide subtree hand-over for the pivot engine (KC_GQ=0 turns it off)
     static const bool gq_on = [] {
@@ -1396,23 +1428,24 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
     cudaEventDestroy(e_fork);
     cudaEventDestroy(e_join);
 
-    std::vector<ull> h(10 + size_t(kSmidSlots));
+    std::vector<ull> h(kOutWords);
     KC_CUDA(cudaMemcpyAsync(h.data(), outs.p, 8 * h.size(), cudaMemcpyDeviceToHost, g->stream));
     if (pivot)
         KC_CUDA(cudaMemcpyAsync(hist, dhist.p, 8 * size_t(L * L), cudaMemcpyDeviceToHost,
                                 g->stream));
     KC_CUDA(cudaStreamSynchronize(g->stream));
+    int gq_ctl[8];
+    memcpy(gq_ctl, &h[kOutGq], sizeof(gq_ctl));
+    // every handed-over subtree must have been walked (its leaves are in hist)
+    KC_REQUIRE(gq_ctl[1] == 0, KC_ECUDA, "subtree queue not drained at kernel exit");
     raw->word_ops = h[8 + kSmidSlots];
     raw->extract_bytes = h[9 + kSmidSlots];
     for (int i = 0; i < 4; ++i) raw->limbs[i] = h[1 + i];
     const ull tri_items = (split && t >= 6) ? ull(n_items_big) : 0ull;
     raw->visits = h[5] + tri_items;  // u's visit of every item split into triples
-    if (p.use_gq && getenv("KC_GQ_DEBUG")) {
-        int c[8] = {0};
-        KC_CUDA(cudaMemcpy(c, gq_ctl.p, 32, cudaMemcpyDeviceToHost));
-        fprintf(stderr, "[kc_gq] pushes=%d pops=%d size=%d hungry=%d busy=%d\n", c[4], c[5], c[1],
-                c[2], c[3]);
-    }
+    if (p.use_gq && getenv("KC_GQ_DEBUG"))
+        fprintf(stderr, "[kc_gq] pushes=%d pops=%d size=%d hungry=%d busy=%d\n", gq_ctl[4],
+                gq_ctl[5], gq_ctl[1], gq_ctl[2], gq_ctl[3]);
     raw->tasks_run = h[6];
     raw->count_ms = ms;
     if (visits_per_sm) {

@@ -60,9 +60,17 @@ class OrientedGraph:
         g = self.graph
         if g._dag_token != self._token:
             info = _lib.KcDagInfo()
-            rank = np.ascontiguousarray(self.ranking.rank, dtype=np.int32)
-            _lib.check(_lib.load().kc_orient(g.handle, _lib.CRIT["given"], _lib._ptr(rank),
-                                             ctypes.byref(info)))
+            r = self.ranking
+            if isinstance(r, _LazyRanking) and r._rank_cache is None:
+                # the permutation was never downloaded and another DAG replaced
+                # this one: every criterion is deterministic, so recompute it
+                # on the device (reading r.rank here would recurse)
+                _lib.check(_lib.load().kc_orient(g.handle, _lib.CRIT[r.criterion], None,
+                                                 ctypes.byref(info)))
+            else:
+                rank = np.ascontiguousarray(r.rank, dtype=np.int32)
+                _lib.check(_lib.load().kc_orient(g.handle, _lib.CRIT["given"], _lib._ptr(rank),
+                                                 ctypes.byref(info)))
             g._dag_token = self._token
         return g.handle
 

@@ -24,6 +24,7 @@ from . import _lib
 from .orientation import CRITERIA, rank_and_orient
 
 ALGORITHMS = ("orient", "pivot")
+SM_SLOTS = 1024  # width of the per-SM visit counters (kc_count's kSmidSlots)
 SCHEMES = ("vertex", "edge")
 _LIMIT_128 = 1 << 128
 
@@ -155,14 +156,22 @@ def device_count_raw(og, cfg: RunConfig, task_lo: int = 0, task_hi: int = -1) ->
     pivot = cfg.algorithm == "pivot"
     dim = og.d_max + 2
     hist = np.zeros(dim * dim, dtype=np.uint64) if pivot else None
-    nsm = _lib.num_sms(og.graph.device)
-    per_sm = np.zeros(1024, dtype=np.uint64)
+    # fixed width (every rank's vector has the same length for the all-reduce);
+    # trimmed to the SMs actually used only when reported (used_sms)
+    per_sm = np.zeros(SM_SLOTS, dtype=np.uint64)
     _lib.check(L.kc_count(h, ctypes.byref(a), ctypes.byref(raw), _lib._ptr(hist),
                           hist.size if pivot else 0, _lib._ptr(per_sm), per_sm.size))
-    used = max(nsm, int(np.flatnonzero(per_sm).max()) + 1 if per_sm.any() else 0)
     return RawCount(np.array(raw.limbs[:], dtype=np.uint64), int(raw.visits), int(raw.tasks_run),
-                    None if hist is None else hist.reshape(dim, dim), per_sm[:used].copy(),
+                    None if hist is None else hist.reshape(dim, dim), per_sm,
                     float(raw.count_ms), int(raw.word_ops), int(raw.extract_bytes))
+
+
+def used_sms(per_sm, nsm: int) -> list:
+    """Per-SM visit counters trimmed to the device's SMs (%smid can exceed the
+    SM count, so a counter above nsm that is non-zero extends the list)."""
+    per_sm = np.asarray(per_sm)
+    used = max(nsm, int(np.flatnonzero(per_sm).max()) + 1 if per_sm.any() else 0)
+    return [int(x) for x in per_sm[:used]]
 
 
 def _binom_checked(n: int, r: int) -> int:
@@ -247,7 +256,7 @@ def run_count(g, cfg: RunConfig) -> CountReport:
     else:
         raw = device_count_raw(og, cfg)
         count, counts = finalize(raw, cfg, g.n, g.m)
-        visits = raw.visits_per_sm.tolist()
+        visits = used_sms(raw.visits_per_sm, nsm)
         dev["count"] = raw.count_ms
         sbytes = scratch_bytes(og, cfg)
         counters = {"word_ops": raw.word_ops, "extract_bytes": raw.extract_bytes,

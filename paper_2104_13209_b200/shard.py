@@ -20,7 +20,7 @@ import numpy as np
 
 from . import _lib
 from .scheduler import CountReport, RawCount, RunConfig, device_count_raw, finalize, load_stats
-from .scheduler import scratch_bytes, validate
+from .scheduler import scratch_bytes, used_sms, validate
 
 
 def balanced_ranges(costs: np.ndarray, world: int) -> list[tuple[int, int]]:
@@ -49,6 +49,27 @@ def task_costs(og, scheme: str) -> np.ndarray:
     costs = np.zeros(max(n.value, 1), dtype=np.int64)
     _lib.check(L.kc_task_costs(h, _lib.SCHEME[scheme], _lib._ptr(costs), n.value))
     return costs[:n.value]
+
+
+def spread_per_rank(raw: RawCount, rank: int, world: int) -> RawCount:
+    """Place this rank's per-SM visit counters in its own slice of a
+    world x SM_SLOTS vector, so the element-wise all-reduce keeps load
+    statistics per (rank, SM) instead of summing SMs of different GPUs."""
+    per = np.asarray(raw.visits_per_sm, dtype=np.uint64)
+    wide = np.zeros(world * per.size, dtype=np.uint64)
+    wide[rank * per.size:(rank + 1) * per.size] = per
+    return RawCount(raw.limbs, raw.visits, raw.tasks_run, raw.hist, wide, raw.count_ms,
+                    raw.word_ops, raw.extract_bytes)
+
+
+def per_rank_sms(wide, world: int, nsm: int) -> list:
+    """Concatenated per-SM counters of every rank (each trimmed to its SMs)."""
+    wide = np.asarray(wide)
+    width = wide.size // max(world, 1)
+    out = []
+    for r in range(world):
+        out += used_sms(wide[r * width:(r + 1) * width], nsm)
+    return out
 
 
 def allreduce_raw(raw: RawCount, group=None) -> RawCount:
@@ -87,12 +108,14 @@ def run_count_sharded(g, cfg: RunConfig, rank: int, world: int, group=None,
     raw = device_count_raw(og, cfg, lo, hi)
     counters = {"word_ops": raw.word_ops, "extract_bytes": raw.extract_bytes,
                 "kernel_ms": raw.count_ms, "tasks_run": raw.tasks_run}
+    nsm = _lib.num_sms(g.device)
+    raw = spread_per_rank(raw, rank, world)
     if world > 1:
         raw = allreduce_raw(raw, group)
     count, counts = finalize(raw, cfg, g.n, g.m)
     count_ms = (time.perf_counter() - t1) * 1000.0
     return CountReport(n=g.n, m=g.m, d_max_undirected=g.max_degree(), d_max=og.d_max, config=cfg,
                        count=count, counts=counts, orient_ms=orient_ms, count_ms=count_ms,
-                       load=load_stats(raw.visits_per_sm.tolist()),
+                       load=load_stats(per_rank_sms(raw.visits_per_sm, world, nsm)),
                        scratch_bytes=scratch_bytes(og, cfg), degeneracy=og.ranking.degeneracy,
                        device_ms={"count": raw.count_ms}, counters=counters)

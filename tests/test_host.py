@@ -16,7 +16,7 @@ from conftest import complete_edges, gnp_edges
 
 from paper_2104_13209_b200 import cli, synth
 from paper_2104_13209_b200.scheduler import RawCount, RunConfig, finalize, make_tasks, validate
-from paper_2104_13209_b200.shard import balanced_ranges
+from paper_2104_13209_b200.shard import balanced_ranges, per_rank_sms, spread_per_rank
 
 
 # ---------------------------------------------------------------- validation
@@ -159,7 +159,17 @@ def _shard_worker(rank, world, port, edges, cfgs, q):
             lo, hi = balanced_ranges(costs, world)[rank]
             c, vis, _ = oracle.run_tasks(og, k, algo, scheme, False, 1, lo, hi)
             raw = _raw_from_count(c, sum(vis))
+            # ranks report different SM usage (rank 1 touches a high %smid):
+            # the all-reduced vector still has one length on every rank
+            per = np.zeros(1024, dtype=np.uint64)
+            per[rank] = sum(vis)
+            if rank == 1:
+                per[700] = 1
+            raw.visits_per_sm = per
+            raw = spread_per_rank(raw, rank, world)
             tot = allreduce_raw(raw)
+            sms = per_rank_sms(tot.visits_per_sm, world, 4)
+            assert len(sms) == 4 + 701 and sms[0] + sms[5] == sum(sms) - 1
             count, _ = finalize(tot, RunConfig(k=k, algorithm=algo, scheme=scheme,
                                                criterion=crit), g.n, g.m)
             out.append((count, tot.visits))
@@ -197,3 +207,17 @@ def test_complete_graph_closed_form_through_finalize():
     count, _ = finalize(_raw_from_count(c), RunConfig(k=6), 70, 2415)
     assert count == c
     assert complete_edges(4).shape == (6, 2)
+
+
+def test_per_rank_sm_counters_keep_ranks_apart():
+    """Advice r1: load statistics per (rank, SM), fixed width for the all-reduce."""
+    a = RawCount(np.zeros(4, dtype=np.uint64), 3, 1, None, np.array([1, 2] + [0] * 1022,
+                                                                   dtype=np.uint64), 0)
+    b = RawCount(np.zeros(4, dtype=np.uint64), 4, 1, None, np.array([5, 0, 0, 7] + [0] * 1020,
+                                                                   dtype=np.uint64), 0)
+    va = spread_per_rank(a, 0, 2).as_vector()
+    vb = spread_per_rank(b, 1, 2).as_vector()
+    assert va.size == vb.size
+    tot = spread_per_rank(a, 0, 2).from_vector(va + vb)
+    assert tot.visits == 7
+    assert per_rank_sms(tot.visits_per_sm, 2, 2) == [1, 2, 5, 0, 0, 7]
