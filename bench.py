@@ -478,76 +478,139 @@ def roofline(kc, g, cfg, rep, a, local):
 # ----------------------------------------------------------------------------
 # CPU baseline / reference arm: the C restatement of the reference
 # ----------------------------------------------------------------------------
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+class CpuBaseline:
+    """The C restatement of the reference (oracle/, pthreads, every host core)
+    timed on a stratified sample of the workload's tasks, projected to the
+    whole graph.
+
+    prepare(): full-graph CSR, ranking (the reference's heap order for
+    degeneracy) and orientation on the CPU -- the ranking + orientation time
+    is measured and charged in full.  Tasks (make_tasks order,
+    scheduler.py:89-95) are sorted by a cost proxy (out-degree for vertex
+    tasks, min(d+(u), d+(v)) for edge tasks) and every `step`-th one is taken
+    (a systematic sample across all strata, heavy tasks included); `step` is
+    calibrated once so a sample costs ~target_s of wall time.
+    measure(): the pool runs the sample with its atomic cursor, heaviest task
+    first (LPT order: balanced); the whole-graph estimate is
+        wall = orient_s + step * sample wall time
+    (each sampled task stands for `step` tasks of its stratum) and value =
+    exact count / wall.  The per-thread CPU-time projection is reported next
+    to it, and the committed whole-graph oracle run of the same workload
+    (tests/golden/scale.json: count, wall, cores, CPU model) as `full_run`."""
+
+    def __init__(self, edges, a, target_s=12.0, workers=None):
+        import oracle
+
+        self.a = a
+        self.workers = workers or os.cpu_count() or 1
+        g = oracle.from_edges(edges)
+        t0 = time.perf_counter()
+        crit = "degeneracy" if a.criterion.startswith("degeneracy") else a.criterion
+        rank, degen = oracle.compute_rank(g, crit)
+        self.og = oracle.orient(g, rank, degen)
+        self.orient_s = time.perf_counter() - t0
+        tasks = oracle.make_tasks(self.og, a.scheme)
+        dout = np.diff(self.og.row_ptr)
+        if a.scheme == "vertex":
+            proxy = dout[tasks]
+        else:
+            proxy = np.minimum(dout[self.og.coo_src[tasks]], dout[self.og.col[tasks]])
+        self.order = tasks[np.argsort(-proxy, kind="stable")]
+        n = max(self.order.size, 1)
+        step0 = max(1, n // 256)
+        t0 = time.perf_counter()
+        self._run(step0)
+        w0 = time.perf_counter() - t0
+        self.step = min(n, max(1, int(w0 * step0 / max(target_s, 1e-9))))
+
+    def _run(self, step):
+        import oracle
+
+        sample = self.order[step // 2::step]
+        c, vis, busy = oracle.run_task_list(self.og, self.a.k, self.a.algo, self.a.scheme,
+                                            sample, self.workers)
+        return c, vis, float(sum(busy)), int(sample.size)
+
+    def measure(self, full_count=None):
+        step = self.step
+        t1 = time.perf_counter()
+        c1, v1, b1, n1 = self._run(step)
+        sample_wall = time.perf_counter() - t1
+        wall = self.orient_s + sample_wall * step
+        count = full_count if full_count is not None else c1 * step
+        rec = {"value": count / wall if wall > 0 else None, "unit": "k-cliques/s",
+               "cores": self.workers, "kind": "port", "cpu_model": _cpu_model(),
+               "sample": (f"oracle/kc_oracle.c worker pool on every {step}-th task of "
+                          f"{self.order.size} sorted by cost proxy ({n1} tasks, "
+                          f"{100.0 / step:.2f}%; {sample_wall:.1f}s wall, {b1:.1f} thread-CPU s)"
+                          f" + full-graph ranking/orientation {self.orient_s:.2f}s"),
+               "estimated_full_wall_s": wall, "orient_s_full": self.orient_s,
+               "estimated_full_wall_s_from_thread_cpu": self.orient_s + b1 * step / self.workers,
+               "sample_count_scaled": str(c1 * step), "sample_visits_scaled": v1 * step,
+               "step": step}
+        rec.update(full_run_record(self.a))
+        return rec
+
+
 def cpu_baseline(edges, a, full_count=None, target_s=12.0, workers=None):
-    """Oracle (C + pthreads, every host core) on a bounded task sample.
+    return CpuBaseline(edges, a, target_s, workers).measure(full_count)
 
-    The sample is a set of small task ranges spread evenly over make_tasks
-    order (ids carry no degree information: RMAT labels are permuted), grown
-    until ~target_s of counting.  Throughput = cliques counted in the sample /
-    (sample count time + the sample's share of the full CPU ranking +
-    orientation time)."""
-    import oracle
 
-    workers = workers or os.cpu_count() or 1
-    g = oracle.from_edges(edges)
-    t0 = time.perf_counter()
-    rank, degen = oracle.compute_rank(g, a.criterion)
-    og = oracle.orient(g, rank, degen)
-    orient_s = time.perf_counter() - t0
-    n_tasks = oracle.num_tasks(og, a.scheme)
-    n_slices = 64
-    stride = max(1, n_tasks // n_slices)
-    width = 1
-    done_tasks, cnt, spent = 0, 0, 0.0
-    covered = [0] * n_slices  # tasks already taken at the head of each slice
-    while spent < target_s and done_tasks < n_tasks:
-        for i in range(n_slices):
-            lo = i * stride + covered[i]
-            hi = min(n_tasks, i * stride + min(stride, covered[i] + width))
-            if i == n_slices - 1:
-                hi = min(n_tasks, lo + width) if lo < n_tasks else lo
-            if lo >= hi:
-                continue
-            t1 = time.perf_counter()
-            c, _, _ = oracle.run_tasks(og, a.k, a.algo, a.scheme, False, workers, lo, hi)
-            spent += time.perf_counter() - t1
-            cnt += c
-            done_tasks += hi - lo
-            covered[i] += hi - lo
-            if spent >= target_s:
-                break
-        width *= 2
-    frac = done_tasks / max(n_tasks, 1)
-    t_eff = spent + orient_s * frac
-    full = frac >= 1.0
-    return {"value": cnt / t_eff if t_eff > 0 else None, "unit": "k-cliques/s",
-            "cores": workers, "kind": "port",
-            "sample": (f"oracle/kc_oracle.c run_tasks on {done_tasks} of {n_tasks} tasks "
-                       f"({100 * frac:.3f}%, {n_slices} evenly spaced ranges), {spent:.1f}s "
-                       f"count + {orient_s:.2f}s orient x frac" + ("; full graph" if full else "")),
-            "sample_count": str(cnt),
-            "full_count_matches": (cnt == full_count) if (full and full_count is not None) else None,
-            "orient_s_full": orient_s}
+def full_run_record(a):
+    """The committed whole-graph oracle run of this exact workload, if any."""
+    try:
+        with open(os.path.join(HERE, "tests", "golden", "scale.json")) as f:
+            recs = json.load(f)
+    except OSError:
+        return {}
+    for r in recs:
+        if (r["workload"], r["k"], r["algorithm"], r["scheme"], r["criterion"]) == (
+                a.workload, a.k, a.algo, a.scheme,
+                "degeneracy" if a.criterion.startswith("degeneracy") else a.criterion) \
+                and not r["all_k"]:
+            wall = r["oracle_orient_s"] + r["oracle_count_s"]
+            return {"full_run": {"count": r["count"], "visits": r["visits"], "wall_s": wall,
+                                 "value": int(r["count"]) / wall, "cores": r["workers"],
+                                 "cpu_model": r["cpu_model"], "source": r["recipe"],
+                                 "when": r["when"]}}
+    return {}
 
 
 def run_reference(a):
+    """The reference arm: the CPU restatement on this host (rank 0 only), on the
+    same workload / metric; each step is one measured sample (CpuBaseline)."""
     world, rank, _ = dist_env()
     if rank != 0:
         return
     edges = workload_edges(a.workload)
     per = max(2.0, min(a.cpu_sample_s, 120.0 / max(a.steps + a.warmup, 1)))
-    for _ in range(a.warmup):
-        cpu_baseline(edges, a, target_s=per / 4)
+    cb = CpuBaseline(edges, a, target_s=per)
+    full = cb.measure()  # warm-up
+    full_count = int(full["full_run"]["count"]) if "full_run" in full else None
+    for _ in range(max(a.warmup - 1, 0)):
+        cb.measure(full_count)
     vals, ms = [], []
     last = None
     for _ in range(a.steps):
         t0 = time.perf_counter()
-        last = cpu_baseline(edges, a, target_s=per)
+        last = cb.measure(full_count)
         ms.append((time.perf_counter() - t0) * 1e3)
         vals.append(last["value"])
     value = float(np.median(vals))
     cpu = dict(last)
     cpu["value"] = value
+    cpu["values_per_step"] = vals
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": "k-cliques/s",
         "n_gpus": world, "steps": a.steps, "warmup": a.warmup,

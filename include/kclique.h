@@ -44,10 +44,13 @@ extern "C" {
 
 /* orientation criteria (orientation.py:9 CRITERIA) */
 #define KC_CRIT_DEGREE 0
-#define KC_CRIT_DEGENERACY 1
+#define KC_CRIT_DEGENERACY 1 /* the reference's sequential heap order (orientation.py:81-113),
+                                rank for rank: core numbers by a bulk peel, then one heap run
+                                per shell-internal component, merged (kc_peel.cu) */
 #define KC_CRIT_GIVEN 2 /* use a caller-provided rank permutation */
-#define KC_CRIT_DEGENERACY_EXACT 3 /* the reference's sequential heap order, exactly
-                                      (orientation.py:81-113); slower than the bulk peel */
+#define KC_CRIT_DEGENERACY_EXACT 3 /* alias of KC_CRIT_DEGENERACY (round-1 name) */
+#define KC_CRIT_DEGENERACY_BULK 4 /* the paper's bulk-synchronous peel order, rank = (round, id):
+                                     a valid degeneracy order but not the heap's */
 
 /* algorithms / schemes (scheduler.py:27-28) */
 #define KC_ALGO_ORIENT 0
@@ -115,8 +118,9 @@ typedef struct {
     double orient_ms;   /* device time of the DAG rebuild */
 } kc_dag_info;
 
-/* criterion KC_CRIT_DEGREE / KC_CRIT_DEGENERACY computed on the device;
- * KC_CRIT_GIVEN uploads rank_in (int32[n] permutation, host). */
+/* criterion KC_CRIT_DEGREE / KC_CRIT_DEGENERACY / KC_CRIT_DEGENERACY_BULK
+ * computed on the device; KC_CRIT_GIVEN uploads rank_in (int32[n]
+ * permutation, host). */
 int kc_orient(kc_graph *g, int criterion, const int32_t *rank_in, kc_dag_info *info);
 /* copy DAG back: rank int32[n], orow_ptr int64[n+1], ocol/ocoo_src int32[m_dir] */
 int kc_dag_download(const kc_graph *g, int32_t *rank, int64_t *orow_ptr, int32_t *ocol,

@@ -20,7 +20,9 @@
  * Word layout is the reference's: uint64 words, LSB-first
  * (_bitops.py:1-5), local index i at bit i%64 of word i/64.
  */
+#define _POSIX_C_SOURCE 200809L
 #include <pthread.h>
+#include <time.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
@@ -628,10 +630,16 @@ typedef struct {
     u64 out[4];
     u64 *slot_lo, *slot_hi;
     u64 meta[2];
+    double busy_s; /* this thread's CPU time */
 } worker_arg;
 
 static void *worker_loop(void *p) {
     worker_arg *a = (worker_arg *)p;
+    {
+        struct timespec ts;
+        clock_gettime(CLOCK_THREAD_CPUTIME_ID, &ts);
+        a->busy_s = (double)ts.tv_sec + 1e-9 * (double)ts.tv_nsec;
+    }
     int64_t cap = a->d_max > 1 ? a->d_max : 1;
     int64_t wcap = (cap + 63) >> 6;
     int64_t *l2g = (int64_t *)malloc(sizeof(int64_t) * (size_t)cap);
@@ -675,6 +683,9 @@ static void *worker_loop(void *p) {
     }
     free(l2g); free(words); free(stk); free(cw); free(cb);
     if (pivot) { free(sc.pruned); free(sc.piv); free(sc.npv); }
+    struct timespec ts;
+    clock_gettime(CLOCK_THREAD_CPUTIME_ID, &ts);
+    a->busy_s = (double)ts.tv_sec + 1e-9 * (double)ts.tv_nsec - a->busy_s;
     return NULL;
 }
 
@@ -690,6 +701,12 @@ static void *worker_loop(void *p) {
  *   flags_out[1] = the cross-worker sum itself exceeded 128 bits.
  *   all_k: slots_lo/hi[d_max+2] (sum over workers, same flags).
  */
+static int run_list(const int64_t *orow_ptr, const int32_t *ocol, const int32_t *ocoo_src,
+                    const int32_t *rank, int64_t d_max, int algo, int edge, int all_k, int64_t t,
+                    const int64_t *tasks, int64_t n_list, int workers, u64 *count_out,
+                    u64 *visits_per_worker, u64 *flags_out, u64 *slots_lo, u64 *slots_hi,
+                    double *busy_s);
+
 int oc_run_tasks(const int64_t *orow_ptr, const int32_t *ocol, const int32_t *ocoo_src,
                  const int32_t *rank, int64_t n, int64_t m_dir, int64_t d_max, int algo, int edge,
                  int all_k, int64_t t, int64_t task_lo, int64_t task_hi, int workers,
@@ -708,6 +725,31 @@ int oc_run_tasks(const int64_t *orow_ptr, const int32_t *ocol, const int32_t *oc
     if (task_lo < 0) task_lo = 0;
     if (task_hi > n_all || task_hi < 0) task_hi = n_all;
     if (task_lo > task_hi) task_lo = task_hi;
+    int rc = run_list(orow_ptr, ocol, ocoo_src, rank, d_max, algo, edge, all_k, t,
+                      tasks + task_lo, task_hi - task_lo, workers, count_out, visits_per_worker,
+                      flags_out, slots_lo, slots_hi, NULL);
+    free(tasks);
+    return rc;
+}
+
+/* The same pool over an explicit list of task ids (vertex ids or oriented
+ * edge ids) -- the CPU baseline's stratified sample.  busy_s (optional,
+ * [workers]) receives each worker thread's CPU time. */
+int oc_run_task_list(const int64_t *orow_ptr, const int32_t *ocol, const int32_t *ocoo_src,
+                     const int32_t *rank, int64_t d_max, int algo, int edge, int all_k, int64_t t,
+                     const int64_t *tasks, int64_t n_list, int workers, u64 *count_out,
+                     u64 *visits_per_worker, u64 *flags_out, u64 *slots_lo, u64 *slots_hi,
+                     double *busy_s) {
+    if (workers < 1) return OC_EINVAL;
+    return run_list(orow_ptr, ocol, ocoo_src, rank, d_max, algo, edge, all_k, t, tasks, n_list,
+                    workers, count_out, visits_per_worker, flags_out, slots_lo, slots_hi, busy_s);
+}
+
+static int run_list(const int64_t *orow_ptr, const int32_t *ocol, const int32_t *ocoo_src,
+                    const int32_t *rank, int64_t d_max, int algo, int edge, int all_k, int64_t t,
+                    const int64_t *tasks, int64_t n_list, int workers, u64 *count_out,
+                    u64 *visits_per_worker, u64 *flags_out, u64 *slots_lo, u64 *slots_hi,
+                    double *busy_s) {
     int pivot = algo != 0 || all_k;
     int64_t bsize = 1;
     u64 *blo = NULL, *bhi = NULL;
@@ -726,7 +768,7 @@ int oc_run_tasks(const int64_t *orow_ptr, const int32_t *ocol, const int32_t *oc
     for (int w = 0; w < workers; w++) {
         worker_arg *a = &args[w];
         a->row_ptr = orow_ptr; a->col = ocol; a->rank = rank; a->coo_src = ocoo_src;
-        a->tasks = tasks + task_lo; a->n_tasks = task_hi - task_lo;
+        a->tasks = tasks; a->n_tasks = n_list;
         a->d_max = d_max; a->t = t; a->edge = edge; a->algo = pivot ? 1 : 0; a->all_k = all_k;
         a->blo = blo; a->bhi = bhi; a->bbig = bbig; a->bsize = bsize;
         a->cursor = &cursor;
@@ -772,8 +814,10 @@ int oc_run_tasks(const int64_t *orow_ptr, const int32_t *ocol, const int32_t *oc
     count_out[1] = (u64)(total >> 64);
     flags_out[0] = (u64)any_over;
     flags_out[1] = (u64)sum_over;
+    if (busy_s)
+        for (int w = 0; w < workers; w++) busy_s[w] = args[w].busy_s;
     for (int w = 0; w < workers; w++) { free(args[w].slot_lo); free(args[w].slot_hi); }
-    free(args); free(th); free(tasks); free(blo); free(bhi); free(bbig);
+    free(args); free(th); free(blo); free(bhi); free(bbig);
     return any_over ? OC_EOVERFLOW : OC_OK;
 }
 

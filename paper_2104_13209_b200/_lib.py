@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libkc.so")
 
 KC_OK, KC_EINVAL, KC_EOVERFLOW, KC_ECUDA, KC_ENOMEM = 0, 1, 3, 4, 5
-CRIT = {"degree": 0, "degeneracy": 1, "given": 2, "degeneracy_exact": 3}
+CRIT = {"degree": 0, "degeneracy": 1, "given": 2, "degeneracy_exact": 3, "degeneracy_bulk": 4}
 ALGO = {"orient": 0, "pivot": 1}
 SCHEME = {"vertex": 0, "edge": 1}
 

@@ -21,7 +21,7 @@ CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 LIB = os.path.join(HERE, "libkc.so")
 BUILD = os.path.join(HERE, "_build")
-SOURCES = ["kc_ingest.cu", "kc_graph.cu", "kc_count.cu", "kc_probe.cu", "kc_api.cu"]
+SOURCES = ["kc_ingest.cu", "kc_graph.cu", "kc_peel.cu", "kc_count.cu", "kc_probe.cu", "kc_api.cu"]
 HEADERS = ["kc_internal.cuh", "kc_traverse.cuh"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -157,7 +157,8 @@ __global__ void k_orient_flags(const int32_t *__restrict__ col, const int32_t *_
 // ctl: [0..2] cnt, [3..5] mn, [6] degeneracy, [7] rounds.
 __global__ void k_peel_coop(const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
                             int64_t n, int32_t *__restrict__ deg, int32_t *__restrict__ round_of,
-                            int32_t *__restrict__ order, int32_t *ctl) {
+                            int32_t *__restrict__ order, int32_t *ctl,
+                            int32_t *__restrict__ core_of) {
     cg::grid_group grid = cg::this_grid();
     const int64_t gtid = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
     const int64_t gsz = int64_t(gridDim.x) * blockDim.x;
@@ -227,7 +228,10 @@ __global__ void k_peel_coop(const int64_t *__restrict__ row_ptr, const int32_t *
             begin_step();
             for (int64_t i = head + gwarp; i < end; i += nwarps) {
                 const int32_t v = order[i];
-                if (lane == 0) round_of[v] = round;
+                if (lane == 0) {
+                    round_of[v] = round;
+                    if (core_of) core_of[v] = level;  // core number = level of removal
+                }
                 for (int64_t e = row_ptr[v] + lane; e < row_ptr[v + 1]; e += 32) {
                     const int32_t w = col[e];
                     if (round_of[w] >= 0) continue;
@@ -252,90 +256,6 @@ __global__ void k_peel_coop(const int64_t *__restrict__ row_ptr, const int32_t *
         ctl[6] = degen;
         ctl[7] = round;
     }
-}
-
-// K3' exact: the reference's sequential peel (orientation.py:81-113) --
-// repeatedly remove the live vertex of minimum (residual degree, id) -- in ONE
-// CTA with a tournament (segment) tree over keys (deg << 32 | v).  Per step
-// the CTA decrements the removed vertex's live neighbours in parallel and
-// repairs only their tree paths, level by level; the top 2^kTopBits leaves'
-// ancestors live in shared memory, the lower levels in global memory (L2).
-constexpr int kExactThreads = 1024;
-constexpr int kTopLevels = 13;  // tree nodes [1, 2^13) in smem (64 KB)
-
-__global__ void __launch_bounds__(kExactThreads)
-    k_peel_exact(const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col, int64_t n,
-                 int levels, uint64_t *__restrict__ tree, uint8_t *__restrict__ removed,
-                 int32_t *__restrict__ dirty, int32_t *__restrict__ order, int32_t *out) {
-    extern __shared__ uint64_t top[];  // nodes [1, 2^kTopLevels)
-    __shared__ int s_nd;
-    const int tid = threadIdx.x;
-    const int64_t N = int64_t(1) << levels;  // leaves at [N, 2N)
-    const int topn = levels < kTopLevels ? int(N) : (1 << kTopLevels);
-    auto node = [&](int64_t i) -> uint64_t & { return i < topn ? top[i] : tree[i]; };
-    // leaves and all internal nodes
-    for (int64_t v = tid; v < N; v += kExactThreads) {
-        uint64_t key = ~0ull;
-        if (v < n) {
-            key = (uint64_t(row_ptr[v + 1] - row_ptr[v]) << 32) | uint64_t(v);
-            removed[v] = 0;
-        }
-        tree[N + v] = key;
-    }
-    __syncthreads();
-    for (int lv = levels - 1; lv >= 0; --lv) {
-        const int64_t lo = int64_t(1) << lv, hi = lo << 1;
-        for (int64_t i = lo + tid; i < hi; i += kExactThreads) {
-            const uint64_t a = (2 * i < topn) ? top[2 * i] : tree[2 * i];
-            const uint64_t b = (2 * i + 1 < topn) ? top[2 * i + 1] : tree[2 * i + 1];
-            const uint64_t m = a < b ? a : b;
-            if (i < topn) top[i] = m;
-            else tree[i] = m;
-        }
-        __syncthreads();
-    }
-    int32_t degen = 0;
-    for (int64_t pos = 0; pos < n; ++pos) {
-        const uint64_t key = node(1);  // uniform read
-        const int32_t v = int32_t(key & 0xffffffffu);
-        const int32_t dv = int32_t(key >> 32);
-        if (tid == 0) {
-            order[pos] = v;
-            removed[v] = 1;
-            tree[N + v] = ~0ull;
-            dirty[0] = v;
-            s_nd = 1;
-        }
-        degen = dv > degen ? dv : degen;
-        __syncthreads();
-        // live neighbours lose one degree (each neighbour appears once in v's list)
-        for (int64_t e = row_ptr[v] + tid; e < row_ptr[v + 1]; e += kExactThreads) {
-            const int32_t w = col[e];
-            if (!removed[w]) {
-                tree[N + w] -= (uint64_t(1) << 32);
-                dirty[atomicAdd(&s_nd, 1)] = w;
-            }
-        }
-        __syncthreads();
-        const int nd = s_nd;
-        // repair the dirty paths bottom-up, one level per barrier
-        for (int lv = levels - 1; lv >= 0; --lv) {
-            for (int i = tid; i < nd; i += kExactThreads) {
-                const int64_t x = (N + dirty[i]) >> (levels - lv);
-                const uint64_t a = node(2 * x), b = node(2 * x + 1);
-                node(x) = a < b ? a : b;
-            }
-            __syncthreads();
-        }
-    }
-    if (tid == 0) out[0] = degen;
-}
-
-__global__ void k_rank_from_order(const int32_t *__restrict__ order, int64_t n,
-                                  int32_t *__restrict__ rank) {
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
-         i += int64_t(gridDim.x) * blockDim.x)
-        rank[order[i]] = int32_t(i);
 }
 
 __global__ void k_peel_keys(const int32_t *__restrict__ round_of, int64_t n, int bits,
@@ -525,8 +445,10 @@ void kc_free_dag(kc_graph *g) {
 }
 
 // K3: bulk peeling.  Returns rank via sort of (round, id); degeneracy = the
-// highest level at which some vertex was removed.
-static void degeneracy_rank(kc_graph *g, int64_t *degeneracy, int64_t *rounds_out) {
+// highest level at which some vertex was removed.  core_of (optional, device
+// int32[n]) receives every vertex's core number.
+static void degeneracy_rank(kc_graph *g, int64_t *degeneracy, int64_t *rounds_out,
+                            int32_t *core_of = nullptr, bool want_rank = true) {
     const int64_t n = g->n;
     KC_REQUIRE(n < (int64_t(1) << 31), KC_EINVAL, "graph too large for 32-bit vertex ids");
     int32_t *deg = kc_alloc<int32_t>(n, g->stream);
@@ -545,13 +467,22 @@ static void degeneracy_rank(kc_graph *g, int64_t *degeneracy, int64_t *rounds_ou
     const int32_t *cl = g->col;
     int64_t nn = n;
     void *args[] = {(void *)&rp, (void *)&cl, (void *)&nn, (void *)&deg, (void *)&round_of,
-                    (void *)&order, (void *)&ctl};
+                    (void *)&order, (void *)&ctl, (void *)&core_of};
     KC_CUDA(cudaLaunchCooperativeKernel((void *)k_peel_coop, dim3(grid), dim3(kPeelThreads), args,
                                         0, g->stream));
     int32_t h[8] = {0};
     KC_CUDA(cudaMemcpyAsync(h, ctl, sizeof(h), cudaMemcpyDeviceToHost, g->stream));
     KC_CUDA(cudaStreamSynchronize(g->stream));
     const int32_t round = h[7];
+    *degeneracy = h[6];
+    *rounds_out = round;
+    if (!want_rank) {
+        kc_free(deg, g->stream);
+        kc_free(round_of, g->stream);
+        kc_free(order, g->stream);
+        kc_free(ctl, g->stream);
+        return;
+    }
     // rank = position in (round, id) order
     int bits = kc_bits_for(n - 1 > 0 ? n - 1 : 1);
     int rbits = kc_bits_for(round > 0 ? round : 1);
@@ -569,45 +500,23 @@ static void degeneracy_rank(kc_graph *g, int64_t *degeneracy, int64_t *rounds_ou
     kc_free(round_of, g->stream);
     kc_free(order, g->stream);
     kc_free(ctl, g->stream);
-    *degeneracy = h[6];
-    *rounds_out = round;
 }
 
-// exact sequential order (reference heap) -> rank = removal position
-static void exact_degeneracy_rank(kc_graph *g, int64_t *degeneracy) {
+// exact sequential order (reference heap, orientation.py:81-113): core
+// numbers from the bulk peel, then the per-shell-component heap runs and
+// their merge (kc_peel.cu)
+static void exact_degeneracy_rank(kc_graph *g, int64_t *degeneracy, int64_t *rounds) {
     const int64_t n = g->n;
-    KC_REQUIRE(n < (int64_t(1) << 31), KC_EINVAL, "graph too large for 32-bit vertex ids");
-    int levels = 0;
-    while ((int64_t(1) << levels) < n) ++levels;
-    const int64_t N = int64_t(1) << levels;
-    uint64_t *tree = kc_alloc<uint64_t>(2 * N, g->stream);
-    uint8_t *removed = kc_alloc<uint8_t>(n, g->stream);
-    int32_t *dirty = kc_alloc<int32_t>(n + 1, g->stream);
-    int32_t *order = kc_alloc<int32_t>(n, g->stream);
-    int32_t *out = kc_alloc<int32_t>(2, g->stream);
-    const int topn = levels < kTopLevels ? int(N) : (1 << kTopLevels);
-    const size_t smem = 8 * size_t(topn);
-    KC_CUDA(cudaFuncSetAttribute(k_peel_exact, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 int(smem)));
-    k_peel_exact<<<1, kExactThreads, smem, g->stream>>>(g->row_ptr, g->col, n, levels, tree,
-                                                        removed, dirty, order, out);
-    KC_CUDA(cudaGetLastError());
-    k_rank_from_order<<<grid_for(n, g->num_sms), kThreads, 0, g->stream>>>(order, n, g->rank);
-    KC_CUDA(cudaGetLastError());
-    int32_t h = 0;
-    KC_CUDA(cudaMemcpyAsync(&h, out, 4, cudaMemcpyDeviceToHost, g->stream));
-    KC_CUDA(cudaStreamSynchronize(g->stream));
-    kc_free(tree, g->stream);
-    kc_free(removed, g->stream);
-    kc_free(dirty, g->stream);
-    kc_free(order, g->stream);
-    kc_free(out, g->stream);
-    *degeneracy = h;
+    int32_t *core = kc_alloc<int32_t>(n, g->stream);
+    degeneracy_rank(g, degeneracy, rounds, core, false);
+    kc_exact_order_from_cores(g, core, *degeneracy, g->rank);
+    kc_free(core, g->stream);
 }
 
 void kc_do_orient(kc_graph *g, int criterion, const int32_t *rank_in, kc_dag_info *info) {
     KC_REQUIRE(criterion == KC_CRIT_DEGREE || criterion == KC_CRIT_DEGENERACY ||
-                   criterion == KC_CRIT_GIVEN || criterion == KC_CRIT_DEGENERACY_EXACT,
+                   criterion == KC_CRIT_GIVEN || criterion == KC_CRIT_DEGENERACY_EXACT ||
+                   criterion == KC_CRIT_DEGENERACY_BULK,
                KC_EINVAL, "unknown orientation criterion");
     KC_REQUIRE(criterion != KC_CRIT_GIVEN || rank_in, KC_EINVAL, "rank_in required");
     kc_free_dag(g);
@@ -630,14 +539,15 @@ void kc_do_orient(kc_graph *g, int criterion, const int32_t *rank_in, kc_dag_inf
             KC_CUDA(cudaStreamSynchronize(g->stream));
             kc_free(keys, g->stream);
             kc_free(keys2, g->stream);
-        } else if (criterion == KC_CRIT_DEGENERACY) {
+        } else if (criterion == KC_CRIT_DEGENERACY_BULK) {
             degeneracy_rank(g, &degen, &rounds);
-        } else if (criterion == KC_CRIT_DEGENERACY_EXACT) {
-            exact_degeneracy_rank(g, &degen);
+        } else if (criterion == KC_CRIT_DEGENERACY || criterion == KC_CRIT_DEGENERACY_EXACT) {
+            exact_degeneracy_rank(g, &degen, &rounds);
         } else {
             KC_CUDA(cudaMemcpyAsync(g->rank, rank_in, 4 * n, cudaMemcpyHostToDevice, g->stream));
         }
-    } else if (criterion == KC_CRIT_DEGENERACY || criterion == KC_CRIT_DEGENERACY_EXACT) {
+    } else if (criterion == KC_CRIT_DEGENERACY || criterion == KC_CRIT_DEGENERACY_EXACT ||
+               criterion == KC_CRIT_DEGENERACY_BULK) {
         degen = 0;
     }
     double rank_ms = t_rank.stop();

@@ -117,6 +117,9 @@ void kc_build_from_csr(kc_graph *g, int64_t n, int64_t m, const int64_t *row_ptr
                        const int32_t *col, const int64_t *orig_ids);
 void kc_do_orient(kc_graph *g, int criterion, const int32_t *rank_in, kc_dag_info *info);
 int64_t kc_task_count(const kc_graph *g, int scheme);
+// exact heap order from core numbers (kc_peel.cu): rank_out int32[n] on the device
+void kc_exact_order_from_cores(kc_graph *g, const int32_t *core, int64_t degeneracy,
+                               int32_t *rank_out);
 void kc_make_tasks(kc_graph *g, int scheme, int64_t lo, int64_t hi, int min_d, int32_t *d_tasks,
                    int64_t *n_out);
 

@@ -4,12 +4,14 @@ Mirrors reference orientation.py: ``CRITERIA``, ``Ranking``,
 ``OrientedGraph``, ``compute_rank``, ``orient``.
 
 * degree: rank by (undirected degree, id) -- identical to orientation.py:124-128.
-* degeneracy: the paper's bulk-synchronous GPU k-core peel (K3).  Every round
-  removes all live vertices of residual degree <= the current level; rank is
-  (round, id).  This is a valid degeneracy order -- d_max equals
-  the degeneracy and counts are identical -- but it is not the sequential
-  heap order of orientation.py:81-113, so per-task visit totals can differ
-  from the reference under this criterion (never under ``degree``).
+* degeneracy: the reference's sequential heap order (orientation.py:81-113),
+  rank for rank, computed in parallel (csrc/kc_peel.cu): core numbers by the
+  bulk k-core peel (K3), then one heap run per connected component of each
+  shell, merged by (core, running-max key).  Visits therefore equal the
+  reference's for every engine.
+* degeneracy_bulk (extension): the paper's bulk-synchronous peel order
+  (PAPER.md:316-321), rank = (round, id) -- a valid degeneracy order
+  (same d_max and counts) but different visits.
 """
 
 from __future__ import annotations
@@ -22,10 +24,12 @@ import numpy as np
 
 from . import _lib
 
-# "degeneracy_exact" (extension): the reference's sequential heap order
-# (orientation.py:81-113) reproduced exactly on the GPU -- identical ranks and
-# therefore identical visits; slower than the bulk peel used by "degeneracy".
-CRITERIA = ("degree", "degeneracy", "degeneracy_exact")
+# "degeneracy" is the reference's sequential heap order (orientation.py:81-113)
+# reproduced exactly on the GPU (identical ranks, hence identical visits);
+# "degeneracy_exact" is its round-1 alias.  "degeneracy_bulk" (extension) is the
+# paper's bulk-synchronous peel order: same degeneracy and counts, different
+# visits, cheaper to compute.
+CRITERIA = ("degree", "degeneracy", "degeneracy_exact", "degeneracy_bulk")
 _token = itertools.count(1)
 
 
