@@ -196,8 +196,7 @@ def run_ours(a):
 
     import paper_2104_13209_b200 as kc
     from paper_2104_13209_b200 import _lib
-    from paper_2104_13209_b200.orientation import rank_and_orient
-    from paper_2104_13209_b200.shard import balanced_ranges, run_count_sharded, task_costs
+    from paper_2104_13209_b200.shard import run_count_sharded
 
     _lib.load()
     edges = workload_edges(a.workload)

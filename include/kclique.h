@@ -14,6 +14,8 @@
  *   kc_orient             <- orientation.py:116-153 compute_rank(g, criterion) + orient(g, ranking)
  *   kc_count              <- scheduler.py:141-185  _worker_loop / _worker_loop_all + the
  *                            thread pool and reduction of scheduler.py:211-293
+ *   kc_num_tasks, kc_task_costs, kc_shard_ranges <- scheduler.py:89-95 make_tasks (+ costs and
+ *                            balanced root ranges for the multi-GPU shards)
  *   kc_extract            <- bitgraph.py:125-152   extract_vertex_induced / extract_edge_induced
  *   kc_count_bitgraph     <- engine_orient.py:91-114, engine_pivot.py:248-308
  *                            count_tcliques_orient / count_tcliques_pivot / ..._all_t
@@ -40,7 +42,7 @@ extern "C" {
 #define KC_ECUDA 4
 #define KC_ENOMEM 5
 
-#define KC_ABI_VERSION 1
+#define KC_ABI_VERSION 2
 
 /* orientation criteria (orientation.py:9 CRITERIA) */
 #define KC_CRIT_DEGREE 0
@@ -152,19 +154,30 @@ typedef struct {
     uint64_t tasks_run;     /* tasks with enough locals */
     int64_t hist_dim;       /* L: hist is L x L u64 (pivot), 0 for orient */
     double count_ms;        /* device time of the counting kernels */
-    double extract_frac;    /* reserved */
+    int32_t group_size;     /* lanes per sub-warp group the orientation warp tier ran with */
+    int32_t launches;       /* counting-kernel launches of this call */
     uint64_t word_ops;      /* roofline: u32 row words ANDed (+POPC) by the traversals */
     uint64_t extract_bytes; /* roofline: global bytes read by the sub-graph builder */
 } kc_count_raw;
 
 /* hist: caller buffer of hist_cap u64 (L*L, L = d_max + 2) or NULL for orient;
- * visits_per_sm: caller buffer of n_sm u64 or NULL. */
+ * visits_per_sm: caller buffer of n_sm u64 or NULL.  Limits: the bitmap
+ * engines hold at most 4096 locals per task (oriented max out-degree <= 4096,
+ * else KC_EINVAL); counts are exact to 2^128 (KC_EOVERFLOW beyond). */
 int kc_count(kc_graph *g, const kc_count_args *args, kc_count_raw *raw, uint64_t *hist,
              int64_t hist_cap, uint64_t *visits_per_sm, int32_t n_sm);
 /* number of make_tasks entries for a scheme (scheduler.py:89-95) */
 int kc_num_tasks(const kc_graph *g, int32_t scheme, int64_t *n_tasks);
-/* per-task cost estimate (int64[n_tasks], make_tasks order) for shard balancing */
-int kc_task_costs(const kc_graph *g, int32_t scheme, int64_t *costs, int64_t n_tasks);
+/* per-task cost estimate (int64[n_tasks], make_tasks order) for shard balancing,
+ * computed on the device for args' scheme / algorithm / k:
+ *   edge tasks (1 + |N+(u) n N+(v)|)^2; vertex tasks of the orientation engine
+ *   at t >= 4 (hub roots split into out-edge items) the sum of their items'
+ *   costs; other vertex tasks d+(v)^2 */
+int kc_task_costs(kc_graph *g, const kc_count_args *args, int64_t *costs, int64_t n_tasks);
+/* root-range shards: cuts int64[world+1], rank r runs [cuts[r], cuts[r+1]) of
+ * make_tasks order, balanced by a prefix sum of kc_task_costs on the device
+ * (only the world+1 cuts cross to the host) */
+int kc_shard_ranges(kc_graph *g, const kc_count_args *args, int32_t world, int64_t *cuts);
 
 /* ---- single-task debug / engine entry points ---------------------- */
 /* bitgraph.py:125-152: l2g int64[cap], words uint64[cap][wpr_cap] (LSB-first) */

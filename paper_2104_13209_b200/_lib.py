@@ -25,7 +25,7 @@ EXPORTS = (
     "kc_abi_version", "kc_last_error", "kc_device_count", "kc_num_sms",
     "kc_normalize_edges", "kc_graph_from_raw_edges", "kc_graph_from_edges", "kc_graph_from_csr", "kc_graph_info", "kc_graph_download",
     "kc_graph_free", "kc_graph_stream", "kc_orient", "kc_dag_download", "kc_count", "kc_num_tasks",
-    "kc_task_costs", "kc_extract", "kc_count_bitgraph", "kc_find_pivot", "kc_probe",
+    "kc_task_costs", "kc_shard_ranges", "kc_extract", "kc_count_bitgraph", "kc_find_pivot", "kc_probe",
 )
 
 
@@ -45,7 +45,8 @@ class KcCountArgs(ctypes.Structure):
 class KcCountRaw(ctypes.Structure):
     _fields_ = [("limbs", ctypes.c_uint64 * 4), ("visits", ctypes.c_uint64),
                 ("tasks_run", ctypes.c_uint64), ("hist_dim", ctypes.c_int64),
-                ("count_ms", ctypes.c_double), ("extract_frac", ctypes.c_double),
+                ("count_ms", ctypes.c_double), ("group_size", ctypes.c_int32),
+                ("launches", ctypes.c_int32),
                 ("word_ops", ctypes.c_uint64), ("extract_bytes", ctypes.c_uint64)]
 
 
@@ -100,7 +101,8 @@ def load(path: str = LIB_PATH):
         "kc_count": (ctypes.c_int, [_P, ctypes.POINTER(KcCountArgs), ctypes.POINTER(KcCountRaw),
                                     _P, _i64, _P, _i32]),
         "kc_num_tasks": (ctypes.c_int, [_P, _i32, ctypes.POINTER(_i64)]),
-        "kc_task_costs": (ctypes.c_int, [_P, _i32, _P, _i64]),
+        "kc_task_costs": (ctypes.c_int, [_P, ctypes.POINTER(KcCountArgs), _P, _i64]),
+        "kc_shard_ranges": (ctypes.c_int, [_P, ctypes.POINTER(KcCountArgs), _i32, _P]),
         "kc_extract": (ctypes.c_int, [_P, _i32, _i64, _i32, _P, _P, _i64, _i64,
                                       ctypes.POINTER(_i64)]),
         "kc_count_bitgraph": (ctypes.c_int, [ctypes.c_int, _P, _i64, _i32, _i32, _i32, _P, _P,
@@ -114,7 +116,7 @@ def load(path: str = LIB_PATH):
         fn = getattr(L, name)
         fn.restype = res
         fn.argtypes = args
-    if L.kc_abi_version() != 1:
+    if L.kc_abi_version() != 2:
         raise ImportError("libkc ABI version mismatch")
     _lib = L
     return L

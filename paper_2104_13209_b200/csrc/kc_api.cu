@@ -281,33 +281,22 @@ int kc_num_tasks(const kc_graph *g, int32_t scheme, int64_t *n_tasks) {
     });
 }
 
-int kc_task_costs(const kc_graph *g, int32_t scheme, int64_t *costs, int64_t n_tasks) {
+int kc_task_costs(kc_graph *g, const kc_count_args *args, int64_t *costs, int64_t n_tasks) {
     return guarded([&] {
-        KC_REQUIRE(g && g->oriented && costs, KC_EINVAL, "graph is not oriented");
-        kc_device_guard guard(g->device);
-        // cost model for shard balancing: d^2 of the root's locals bound
-        std::vector<int64_t> orow(g->n + 1);
-        KC_CUDA(cudaMemcpy(orow.data(), g->orow_ptr, 8 * (g->n + 1), cudaMemcpyDeviceToHost));
-        if (scheme == KC_SCHEME_VERTEX) {
-            int64_t i = 0;
-            for (int64_t v = 0; v < g->n && i < n_tasks; ++v) {
-                int64_t d = orow[v + 1] - orow[v];
-                if (d > 0) costs[i++] = d * d;
-            }
-            KC_REQUIRE(i == n_tasks, KC_EINVAL, "n_tasks does not match make_tasks");
-        } else {
-            KC_REQUIRE(n_tasks == g->m_dir, KC_EINVAL, "n_tasks does not match make_tasks");
-            std::vector<int32_t> src(g->m_dir), dst(g->m_dir);
-            if (g->m_dir) {
-                KC_CUDA(cudaMemcpy(src.data(), g->ocoo, 4 * g->m_dir, cudaMemcpyDeviceToHost));
-                KC_CUDA(cudaMemcpy(dst.data(), g->ocol, 4 * g->m_dir, cudaMemcpyDeviceToHost));
-            }
-            for (int64_t e = 0; e < g->m_dir; ++e) {
-                int64_t a = orow[src[e] + 1] - orow[src[e]], b = orow[dst[e] + 1] - orow[dst[e]];
-                int64_t d = a < b ? a : b;
-                costs[e] = d * d;
-            }
-        }
+        KC_REQUIRE(g && g->oriented && args && (costs || n_tasks == 0), KC_EINVAL,
+                   "graph is not oriented");
+        KC_REQUIRE(args->scheme == KC_SCHEME_VERTEX || args->scheme == KC_SCHEME_EDGE, KC_EINVAL,
+                   "unknown scheme");
+        kc_do_task_costs(g, args, costs, n_tasks);
+    });
+}
+
+int kc_shard_ranges(kc_graph *g, const kc_count_args *args, int32_t world, int64_t *cuts) {
+    return guarded([&] {
+        KC_REQUIRE(g && g->oriented && args && cuts, KC_EINVAL, "graph is not oriented");
+        KC_REQUIRE(args->scheme == KC_SCHEME_VERTEX || args->scheme == KC_SCHEME_EDGE, KC_EINVAL,
+                   "unknown scheme");
+        kc_do_shard_ranges(g, args, world, cuts);
     });
 }
 

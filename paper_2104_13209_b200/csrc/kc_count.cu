@@ -53,9 +53,10 @@ struct CountParams {
     ull *overflow_n;
     kct::GQueue gq;      // pivot: GPU-wide subtree queue of the warp-tier kernel
     int use_gq;
+    int gq_push_min, gq_cooldown, gq_room;  // hand-over policy (kct::PivotLeafSink)
     int dcap;          // max locals per task
     int wcap;          // ceil(dcap / 32)
-    int group_size;    // reserved (sub-warp group size; traversal is warp-granular)
+    int group_size;    // orientation warp tier: lanes per sub-warp group (1..32)
     int rows_in_smem;  // rows in shared memory, else in rows_global slot
     uint32_t *rows_global;
     int64_t rows_slot;   // u32 words per CTA slot
@@ -414,6 +415,9 @@ __global__ void __launch_bounds__(BLOCK) k_count(CountParams p) {
     sink.eager = true;  // CTA tier
     sink.l2g = l2g;
     sink.hc = s_hc + 2 * warp;
+    sink.push_min = p.gq_push_min;
+    sink.cooldown = p.gq_cooldown;
+    sink.room_min = p.gq_room;
     if ((tid & 31) == 0) {
         sink.hc[0] = 0;
         sink.hc[1] = 0;
@@ -495,6 +499,7 @@ __global__ void __launch_bounds__(BLOCK) k_count(CountParams p) {
 constexpr int kWarpD = 128;
 constexpr int kGqCap = 4096;  // GPU-wide subtree queue slots (pivot)
 constexpr int kSplitD = 32;  // orientation/vertex: roots above this are split into edge items
+constexpr int kAutoGroup = 8;  // orientation sub-warp group size for group_size = 0
 
 
 // warp-level bit matrix of the sub-graph induced by the sorted vertices l2g[0..d)
@@ -562,7 +567,7 @@ __device__ int warp_build(const CountParams &p, int32_t task, int32_t *l2g, uint
     return d;
 }
 
-template <int BLOCK, int MODE, bool GQ>
+template <int BLOCK, int MODE, bool GQ, int G = 32>
 __global__ void __launch_bounds__(BLOCK) k_count_warp(CountParams p) {
     constexpr int NW = BLOCK / 32;
     constexpr int D = kWarpD, WPL = 1;
@@ -600,6 +605,9 @@ __global__ void __launch_bounds__(BLOCK) k_count_warp(CountParams p) {
     sink.eager = false;
     sink.l2g = l2g;
     sink.hc = s_hc + 2 * warp;
+    sink.push_min = p.gq_push_min;
+    sink.cooldown = p.gq_cooldown;
+    sink.room_min = p.gq_room;
     for (int i = lane; i < hist_cells; i += 32) whist[i] = 0;
     if (lane == 0) {
         sink.hc[0] = 0;
@@ -656,14 +664,14 @@ __global__ void __launch_bounds__(BLOCK) k_count_warp(CountParams p) {
                     work += 1;
                 }
             } else if (W == 1) {
-                kct::orient_small(rows, all, 0, last, SS.sstk, lane, acc, visits, work);
+                kct::orient_small<G>(rows, all, 0, last, SS.sstk, lane, acc, visits, work);
             } else {
                 for (int u = 0; u < d; ++u) {
                     if (lane == 0) {
                         ++visits;
                         work += 1;
                     }
-                    kct::orient_subtree<WPL>(rows, RS, W, last, u, F, list, cbuf, SS, acc, visits,
+                    kct::orient_subtree<WPL, G>(rows, RS, W, last, u, F, list, cbuf, SS, acc, visits,
                                              work);
                 }
             }
@@ -958,6 +966,7 @@ inline int grid_1d(int64_t n, int sms) {
 
 // stream of the current library call: DevBuf allocations are stream-ordered on it
 thread_local cudaStream_t tl_stream = nullptr;
+thread_local int tl_launches = 0;  // counting-kernel launches of the current call
 struct StreamScope {
     cudaStream_t prev;
     explicit StreamScope(cudaStream_t s) : prev(tl_stream) { tl_stream = s; }
@@ -1127,6 +1136,7 @@ void launch_wpl(kc_graph *g, CountParams &p, int grid_override, Keep &keep,
     order_after_allocs(g, stream);
     kern<<<grid, kBlock, smem, stream>>>(p);
     KC_CUDA(cudaGetLastError());
+    ++tl_launches;
 }
 
 // warp-per-task kernel for tasks with at most kWarpD locals
@@ -1143,6 +1153,19 @@ void launch_warp(kc_graph *g, CountParams &p, Keep &keep, cudaStream_t stream) {
     const size_t smem = 4 * size_t(NW) * (fixed + size_t(nsm) * p.fw) + 64;
     auto kern = (MODE == MODE_PIVOT && p.use_gq) ? k_count_warp<kBlock, MODE, true>
                                                  : k_count_warp<kBlock, MODE, false>;
+    if constexpr (MODE == MODE_ORIENT) {
+        // orientation: sub-warp group size; the pivot
+        // engine scores candidates one lane each (group size 1 in the
+        // paper's terms, its favourable setting per PAPER.md:720)
+        switch (p.group_size) {
+            case 1: kern = k_count_warp<kBlock, MODE, false, 1>; break;
+            case 2: kern = k_count_warp<kBlock, MODE, false, 2>; break;
+            case 4: kern = k_count_warp<kBlock, MODE, false, 4>; break;
+            case 8: kern = k_count_warp<kBlock, MODE, false, 8>; break;
+            case 16: kern = k_count_warp<kBlock, MODE, false, 16>; break;
+            default: kern = k_count_warp<kBlock, MODE, false, 32>; break;
+        }
+    }
     KC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     int per_sm = 0;
     KC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBlock, smem));
@@ -1160,6 +1183,7 @@ void launch_warp(kc_graph *g, CountParams &p, Keep &keep, cudaStream_t stream) {
     order_after_allocs(g, stream);
     kern<<<grid, kBlock, smem, stream>>>(p);
     KC_CUDA(cudaGetLastError());
+    ++tl_launches;
 }
 
 template <int MODE>
@@ -1208,6 +1232,7 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
     if (visits_per_sm) memset(visits_per_sm, 0, sizeof(uint64_t) * size_t(n_sm));
     kc_device_guard guard(g->device);
     StreamScope scope(g->stream);
+    tl_launches = 0;
 
     int64_t all = kc_task_count(g, a->scheme);
     int64_t lo = a->task_lo < 0 ? 0 : a->task_lo;
@@ -1260,7 +1285,7 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
     p.all_k = a->all_k;
     p.dcap = int(std::max<int64_t>(g->d_max, 1));
     p.wcap = (p.dcap + 31) / 32;
-    p.group_size = gs;
+    p.group_size = gs == 0 ? kAutoGroup : gs;
     p.hist_dim = int(L);
     p.hist = dhist.as<ull>();
     p.sh_hl = int(std::min<int64_t>(L, 48));
@@ -1291,6 +1316,13 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
         return !(e && e[0] == '0');  // on unless KC_GQ=0
     }();
     p.use_gq = pivot && gq_on ? 1 : 0;
+    auto env_int = [](const char *name, int dflt) {
+        const char *e = getenv(name);
+        return e && *e ? atoi(e) : dflt;
+    };
+    p.gq_push_min = env_int("KC_GQ_PUSHMIN", kct::kPushMin);
+    p.gq_cooldown = env_int("KC_GQ_COOLDOWN", kct::kPushCooldown);
+    p.gq_room = env_int("KC_GQ_ROOM", kct::kPushRoom);
     Keep keep;
     // Edge tasks (and split items) all go to the warp-per-task kernel; the few
     // whose intersection exceeds kWarpD locals are appended to an overflow
@@ -1448,10 +1480,149 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
                 gq_ctl[5], gq_ctl[1], gq_ctl[2], gq_ctl[3]);
     raw->tasks_run = h[6];
     raw->count_ms = ms;
+    raw->group_size = pivot ? 1 : p.group_size;
+    raw->launches = tl_launches;
     if (visits_per_sm) {
         for (int i = 0; i < n_sm && i < kSmidSlots; ++i) visits_per_sm[i] = h[8 + i];
         if (n_sm > 0) visits_per_sm[0] += tri_items;  // see raw->visits
     }
+}
+
+namespace {
+// per-task cost estimate for shard balancing, make_tasks order (scheduler.py:89-95)
+//   vertex tasks, orientation t >= 4 (hub roots split into out-edge items):
+//       sum over out-edges e of (1 + |N+(u) n N+(v)|)^2     (the split items' cost)
+//   other vertex tasks: d+(v)^2;   edge tasks: (1 + |N+(u) n N+(v)|)^2
+__global__ void k_vertex_cost(const int64_t *__restrict__ orow, const int32_t *__restrict__ esize,
+                              int64_t n, int64_t *__restrict__ cost) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
+    const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t v = warp; v < n; v += nw) {
+        const int64_t b = orow[v], e = orow[v + 1];
+        int64_t c = 0;
+        if (esize) {
+            for (int64_t i = b + lane; i < e; i += 32) {
+                const int64_t x = 1 + esize[i];
+                c += x * x;
+            }
+            for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+        } else {
+            c = (e - b) * (e - b);
+        }
+        if (lane == 0) cost[v] = c;
+    }
+}
+
+__global__ void k_edge_cost(const int32_t *__restrict__ esize, int64_t m, int64_t *__restrict__ cost) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t x = 1 + esize[i];
+        cost[i] = x * x;
+    }
+}
+
+// cuts[r] = 1 + first i with cum[i] >= total * r / world (shard.balanced_ranges)
+__global__ void k_cuts(const int64_t *__restrict__ cum, int64_t n, int world, int64_t *cuts) {
+    const double total = double(cum[n - 1]);
+    for (int r = threadIdx.x + 1; r < world; r += blockDim.x) {
+        const double target = total * double(r) / double(world);
+        int64_t lo = 0, hi = n;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (double(cum[mid]) < target) lo = mid + 1;
+            else hi = mid;
+        }
+        cuts[r] = lo + 1;
+    }
+}
+}  // namespace
+
+// device task costs in make_tasks order; returns the task count, costs in *out
+static int64_t device_task_costs(kc_graph *g, const kc_count_args *a, DevBuf &out) {
+    const bool pivot = a->algorithm == KC_ALGO_PIVOT;
+    const int t = a->scheme == KC_SCHEME_VERTEX ? a->k - 1 : a->k - 2;
+    const bool split = !pivot && a->scheme == KC_SCHEME_VERTEX && t >= 4;
+    if ((split || a->scheme == KC_SCHEME_EDGE) && !g->esize && g->m_dir > 0) {
+        g->esize = kc_alloc<int32_t>(g->m_dir, g->stream);
+        k_edge_sizes<<<g->num_sms * 16, 256, 0, g->stream>>>(g->orow_ptr, g->ocol, g->ocoo,
+                                                             g->m_dir, g->esize);
+        KC_CUDA(cudaGetLastError());
+    }
+    if (a->scheme == KC_SCHEME_EDGE) {
+        new (&out) DevBuf(8 * size_t(std::max<int64_t>(g->m_dir, 1)));
+        if (g->m_dir)
+            k_edge_cost<<<grid_1d(g->m_dir, g->num_sms), 256, 0, g->stream>>>(
+                g->esize, g->m_dir, out.as<int64_t>());
+        KC_CUDA(cudaGetLastError());
+        return g->m_dir;
+    }
+    const int64_t n = g->n;
+    if (n == 0) {
+        new (&out) DevBuf(8);
+        return 0;
+    }
+    DevBuf cost(8 * size_t(n)), flag(4 * size_t(n)), cnt(8);
+    k_vertex_cost<<<g->num_sms * 16, 256, 0, g->stream>>>(g->orow_ptr, split ? g->esize : nullptr,
+                                                          n, cost.as<int64_t>());
+    k_vertex_flags<<<grid_1d(n, g->num_sms), 256, 0, g->stream>>>(g->orow_ptr, n,
+                                                                   flag.as<int32_t>());
+    new (&out) DevBuf(8 * size_t(n));
+    size_t bytes = 0;
+    KC_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, cost.as<int64_t>(), flag.as<int32_t>(),
+                                       out.as<int64_t>(), cnt.as<int32_t>(), int(n), g->stream));
+    void *tmp = kc_tmp(g, bytes);
+    KC_CUDA(cub::DeviceSelect::Flagged(tmp, bytes, cost.as<int64_t>(), flag.as<int32_t>(),
+                                       out.as<int64_t>(), cnt.as<int32_t>(), int(n), g->stream));
+    int32_t h = 0;
+    KC_CUDA(cudaMemcpyAsync(&h, cnt.p, 4, cudaMemcpyDeviceToHost, g->stream));
+    KC_CUDA(cudaStreamSynchronize(g->stream));
+    return h;
+}
+
+void kc_do_task_costs(kc_graph *g, const kc_count_args *a, int64_t *costs, int64_t n_tasks) {
+    KC_REQUIRE(g->oriented, KC_EINVAL, "graph is not oriented");
+    kc_device_guard guard(g->device);
+    StreamScope scope(g->stream);
+    DevBuf out;
+    const int64_t n = device_task_costs(g, a, out);
+    KC_REQUIRE(n == n_tasks, KC_EINVAL, "n_tasks does not match make_tasks");
+    if (n)
+        KC_CUDA(cudaMemcpyAsync(costs, out.p, 8 * size_t(n), cudaMemcpyDeviceToHost, g->stream));
+    KC_CUDA(cudaStreamSynchronize(g->stream));
+}
+
+void kc_do_shard_ranges(kc_graph *g, const kc_count_args *a, int world, int64_t *cuts) {
+    KC_REQUIRE(g->oriented, KC_EINVAL, "graph is not oriented");
+    KC_REQUIRE(world >= 1, KC_EINVAL, "world must be >= 1");
+    kc_device_guard guard(g->device);
+    StreamScope scope(g->stream);
+    DevBuf cost;
+    const int64_t n = device_task_costs(g, a, cost);
+    std::vector<int64_t> h(size_t(world) + 1, 0);
+    h[world] = n;
+    if (world > 1 && n > 0) {
+        DevBuf cum(8 * size_t(n)), dc(8 * (size_t(world) + 1));
+        size_t bytes = 0;
+        KC_CUDA(cub::DeviceScan::InclusiveSum(nullptr, bytes, cost.as<int64_t>(),
+                                              cum.as<int64_t>(), int(n), g->stream));
+        void *tmp = kc_tmp(g, bytes);
+        KC_CUDA(cub::DeviceScan::InclusiveSum(tmp, bytes, cost.as<int64_t>(), cum.as<int64_t>(),
+                                              int(n), g->stream));
+        k_cuts<<<1, 128, 0, g->stream>>>(cum.as<int64_t>(), n, world, dc.as<int64_t>());
+        KC_CUDA(cudaGetLastError());
+        KC_CUDA(cudaMemcpyAsync(h.data() + 1, dc.as<int64_t>() + 1, 8 * size_t(world - 1),
+                                cudaMemcpyDeviceToHost, g->stream));
+        KC_CUDA(cudaStreamSynchronize(g->stream));
+    } else if (world > 1) {
+        for (int r = 1; r < world; ++r) h[r] = 0;
+    }
+    for (int r = 0; r <= world; ++r) {  // clip + monotone, as shard.balanced_ranges
+        h[r] = std::min(std::max<int64_t>(h[r], 0), n);
+        if (r > 0) h[r] = std::max(h[r], h[r - 1]);
+    }
+    h[world] = n;
+    memcpy(cuts, h.data(), 8 * (size_t(world) + 1));
 }
 
 void kc_do_extract(kc_graph *g, int scheme, int64_t task, int directed, int64_t *l2g,

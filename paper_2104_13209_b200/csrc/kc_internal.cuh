@@ -126,6 +126,8 @@ void kc_make_tasks(kc_graph *g, int scheme, int64_t lo, int64_t hi, int min_d, i
 // counting (kc_count.cu)
 void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_t *hist,
                  int64_t hist_cap, uint64_t *visits_per_sm, int32_t n_sm);
+void kc_do_task_costs(kc_graph *g, const kc_count_args *a, int64_t *costs, int64_t n_tasks);
+void kc_do_shard_ranges(kc_graph *g, const kc_count_args *a, int world, int64_t *cuts);
 void kc_do_extract(kc_graph *g, int scheme, int64_t task, int directed, int64_t *l2g,
                    uint64_t *words, int64_t cap, int64_t wpr_cap, int64_t *d_out);
 void kc_do_count_bitgraph(int device, const uint64_t *rows, int64_t d, int t, int algorithm,

@@ -393,6 +393,172 @@ __device__ __forceinline__ int compress(const uint32_t *__restrict__ rows, int R
     return n;
 }
 
+// ---------------------------------------------------------------------------
+// Sub-warp groups for the orientation engine's S-tier.
+//
+// In a compressed (<= 32 member) subtree the levels above the last two are
+// walked by the whole warp as uniform scalar code; the last two levels --
+// where almost all visits are -- are split over sub-warp groups of G lanes
+// (G = 32, 16, 8, 4, 2, 1): at a frame (C, R) of level last-2 the 32/G groups
+// take different children v of R (id stripes), and the G lanes of a group
+// split the members x of that child's set X = C & row(v) (id stripes again);
+// each lane adds popc(X & row x & row y) over y in X & row x through the
+// carry-save accumulator.  G = 32 is one child at a time over the whole warp
+// (pairs_small); G = 1 is one child per lane.  Counts and visits are sums, so
+// they do not depend on G (engine_orient.py:32-79: visit = node expanded,
+// last level = popcount).
+// ---------------------------------------------------------------------------
+template <int NW>
+struct Bits {
+    uint32_t w[NW];
+};
+
+template <int NW>
+__device__ __forceinline__ Bits<NW> bits_all(int d) {
+    Bits<NW> b;
+#pragma unroll
+    for (int i = 0; i < NW; ++i) {
+        const int lo = i << 5;
+        b.w[i] = lo >= d ? 0u : (lo + 32 <= d ? FULL : ((1u << (d - lo)) - 1u));
+    }
+    return b;
+}
+
+template <int NW>
+__device__ __forceinline__ Bits<NW> bits_row(const uint32_t *__restrict__ rows, int v) {
+    Bits<NW> b;
+    if (NW == 4) {
+        const uint4 r = *reinterpret_cast<const uint4 *>(rows + (v << 2));
+        b.w[0] = r.x;
+        b.w[NW > 1 ? 1 : 0] = r.y;
+        b.w[NW > 2 ? 2 : 0] = r.z;
+        b.w[NW > 3 ? 3 : 0] = r.w;
+    } else {
+        b.w[0] = rows[v];
+    }
+    return b;
+}
+
+template <int NW>
+__device__ __forceinline__ Bits<NW> bits_and(const Bits<NW> &a, const Bits<NW> &b) {
+    Bits<NW> c;
+#pragma unroll
+    for (int i = 0; i < NW; ++i) c.w[i] = a.w[i] & b.w[i];
+    return c;
+}
+
+template <int NW>
+__device__ __forceinline__ bool bits_any(const Bits<NW> &a) {
+    uint32_t x = 0;
+#pragma unroll
+    for (int i = 0; i < NW; ++i) x |= a.w[i];
+    return x != 0;
+}
+
+template <int NW>
+__device__ __forceinline__ unsigned bits_popc(const Bits<NW> &a) {
+    unsigned c = 0;
+#pragma unroll
+    for (int i = 0; i < NW; ++i) c += unsigned(__popc(a.w[i]));
+    return c;
+}
+
+// highest member, removed from a (a must be nonempty)
+template <int NW>
+__device__ __forceinline__ int bits_pop_top(Bits<NW> &a) {
+#pragma unroll
+    for (int i = NW - 1; i > 0; --i) {
+        if (a.w[i]) {
+            const int b = 31 - __clz(a.w[i]);
+            a.w[i] ^= 1u << b;
+            return (i << 5) + b;
+        }
+    }
+    const int b = 31 - __clz(a.w[0]);
+    a.w[0] ^= 1u << b;
+    return b;
+}
+
+// bits b of a 32-bit word with b % n == r (n a power of two dividing 32)
+__device__ __forceinline__ uint32_t stripe32(int n, int r) {
+    uint32_t m = 0;
+    for (int b = r; b < 32; b += n) m |= 1u << b;
+    return m;
+}
+
+template <int NW>
+__device__ __forceinline__ Bits<NW> bits_stripe(const Bits<NW> &a, uint32_t s) {
+    Bits<NW> c;
+#pragma unroll
+    for (int i = 0; i < NW; ++i) c.w[i] = a.w[i] & s;
+    return c;
+}
+
+template <int NW>
+__device__ __forceinline__ Bits<NW> bits_shfl(const Bits<NW> &a, int src) {
+    Bits<NW> c;
+#pragma unroll
+    for (int i = 0; i < NW; ++i) c.w[i] = __shfl_sync(FULL, a.w[i], src);
+    return c;
+}
+
+// the last two levels below the members xs of X (xs = this lane's share):
+// per x a visit, X & row x its child set (each member a visit), and
+// popc(X & row x & row y) cliques per y in it
+template <int NW>
+__device__ __forceinline__ void score_share(const uint32_t *__restrict__ rows, const Bits<NW> &X,
+                                            Bits<NW> xs, unsigned &a, unsigned &vs) {
+    while (bits_any<NW>(xs)) {
+        const int x = bits_pop_top<NW>(xs);
+        const Bits<NW> cm = bits_and<NW>(X, bits_row<NW>(rows, x));
+        vs += 1u + bits_popc<NW>(cm);
+        CsaAcc h;
+        Bits<NW> m = cm;
+        if (NW == 1) {
+            uint32_t mm = m.w[0];
+            while (mm) {  // two members per trip: independent loads in flight
+                const int y0 = 31 - __clz(mm);
+                mm ^= 1u << y0;
+                const uint32_t r0 = rows[y0];
+                uint32_t r1 = 0;
+                if (mm) {
+                    const int y1 = 31 - __clz(mm);
+                    mm ^= 1u << y1;
+                    r1 = rows[y1];
+                }
+                h.add2(cm.w[0] & r0, cm.w[0] & r1);
+            }
+        } else {
+            while (bits_any<NW>(m)) {
+                const int y = bits_pop_top<NW>(m);
+                const Bits<NW> r = bits_row<NW>(rows, y);
+                h.add4(cm.w[0] & r.w[0], cm.w[NW > 1 ? 1 : 0] & r.w[NW > 1 ? 1 : 0],
+                       cm.w[NW > 2 ? 2 : 0] & r.w[NW > 2 ? 2 : 0],
+                       cm.w[NW > 3 ? 3 : 0] & r.w[NW > 3 ? 3 : 0]);
+            }
+        }
+        a += h.total();
+    }
+}
+
+// children v of R under frame C (level last-2), split over sub-warp groups
+template <int G, int NW>
+__device__ __forceinline__ void pair_batch(const uint32_t *__restrict__ rows, const Bits<NW> &C,
+                                           const Bits<NW> &R, int lane, ull &acc, ull &visits) {
+    constexpr int NG = 32 / G;
+    const Bits<NW> mine = bits_stripe<NW>(R, stripe32(NG, lane / G));
+    const uint32_t xstripe = stripe32(G, lane % G);
+    unsigned a = 0, vs = 0;
+    Bits<NW> gen = mine;
+    while (bits_any<NW>(gen)) {
+        const int v = bits_pop_top<NW>(gen);
+        const Bits<NW> X = bits_and<NW>(C, bits_row<NW>(rows, v));
+        score_share<NW>(rows, X, bits_stripe<NW>(X, xstripe), a, vs);
+    }
+    acc += a;
+    visits += vs;
+}
+
 // orientation, last two levels over compressed set C (C = frame last-1)
 __device__ __forceinline__ void pairs_small(const uint32_t *srow, uint32_t C, int lane, ull &acc,
                                             ull &visits, ull &work) {
@@ -425,6 +591,7 @@ __device__ __forceinline__ void pairs_small(const uint32_t *srow, uint32_t C, in
 // The scalar frame stack lives in registers: lane j holds frame s0+j (the
 // depth of a <= 32-member subtree is < 32), pushed with a predicated move and
 // popped with two shuffles -- no shared memory, no warp barrier.
+template <int G = 32>
 __device__ void orient_small(const uint32_t *srow, uint32_t C, int s, int last, uint32_t *sstk,
                              int lane, ull &acc, ull &visits, ull &work) {
     (void)sstk;
@@ -438,6 +605,18 @@ __device__ void orient_small(const uint32_t *srow, uint32_t C, int s, int last, 
     uint32_t fC = 0, fR = 0;  // this lane's frame (depth s0 + lane)
     unsigned uvis = 0;        // uniform visit count of the sequential levels
     for (;;) {
+        if (G < 32 && s + 2 == last) {
+            // the children of this frame are scored by sub-warp groups
+            const ull v0 = visits;
+            Bits<1> c1, r1;
+            c1.w[0] = C;
+            r1.w[0] = R;
+            pair_batch<G, 1>(srow, c1, r1, lane, acc, visits);
+            work += visits - v0;
+            uvis += unsigned(__popc(R));
+            R = 0;
+            __syncwarp();
+        }
         if (R == 0) {
             if (s == s0) break;
             --s;
@@ -532,20 +711,21 @@ struct PivotLeafSink {
     bool eager;          // CTA tier: push large children without rate limit
     const int32_t *l2g;  // local id -> global vertex id of the current universe
     int *hc;             // per-warp smem: [0] countdown [1] cached hungry
+    int push_min = kPushMin, cooldown = kPushCooldown, room_min = kPushRoom;
     // uniform: should a child of n members be handed to a hungry warp?
     // Rate-limited: at most one hand-over per kPushCooldown decisions, so a
     // donor keeps doing its own work and thieves get substantial subtrees.
     __device__ __forceinline__ bool want_push(int n, int room, int lane) const {
-        if (!gq || n < kPushMin || n > kGItemMax) return false;
+        if (!gq || n < push_min || n > kGItemMax) return false;
         if (eager) {
             // CTA tier: hand every large (L-tier) child to a hungry warp-tier
             // warp -- its W <= 4 universe walks it far cheaper than this one
             if (n <= 32) return false;
-        } else if (room < kPushRoom) {
+        } else if (room < room_min) {
             return false;  // shallow remaining tree: cheaper to walk
         }
         if (lane == 0 && --hc[0] <= 0) {
-            hc[0] = eager ? 16 : kPushCooldown;
+            hc[0] = eager ? 16 : cooldown;
             hc[1] = gq->vol(2);
         }
         __syncwarp();
@@ -666,7 +846,7 @@ __device__ __forceinline__ void donate_bottom(const uint32_t *srow, const int *m
         ++uvis;
         return;
     }
-    if (__popc(X) >= kPushMin && sink.push_compressed(srow, X, sj + 1, np2, lane)) {
+    if (__popc(X) >= sink.push_min && sink.push_compressed(srow, X, sj + 1, np2, lane)) {
         ++uvis;
         return;
     }
@@ -715,7 +895,7 @@ __device__ void pivot_small(const uint32_t *srow, uint32_t myrow, uint32_t C, in
             // GPU-wide work sharing: while some warp is hungry, donate the
             // SHALLOWEST pending branch (the biggest subtree this warp still
             // owns), classic work stealing from the bottom of the stack
-            if (sink.gq && s > s0 && sink.want_push(kPushMin, allk ? 1 << 20 : t - s0, lane))
+            if (sink.gq && s > s0 && sink.want_push(sink.push_min, allk ? 1 << 20 : t - s0, lane))
                 donate_bottom(srow, map, s - s0, s0, t, allk, fC, fP, fR, fPN, sink, lane, uvis);
             if (lane == s - s0) {
                 fC = C;
@@ -768,25 +948,25 @@ constexpr int kSmallWords = 32 + 5 * kSmallDepth;
 // ---------------------------------------------------------------------------
 // hand a set X at frame s (s <= last-1) to the S-tier if it has <= 32
 // members; returns false (nothing done) otherwise
-template <int WPL>
+template <int WPL, int G = 32>
 __device__ __forceinline__ bool orient_try_small(const uint32_t *__restrict__ rows, int RS, int W,
                                                  const Set<WPL> &X, int s, int last, int *list,
                                                  const SmallScratch &S, int lane, ull &acc,
                                                  ull &visits, ull &work) {
     if (W == 1) {  // rows are already one word: identity relabelling
-        orient_small(rows, __shfl_sync(FULL, X.w[0], 0), s, last, S.sstk, lane, acc, visits,
+        orient_small<G>(rows, __shfl_sync(FULL, X.w[0], 0), s, last, S.sstk, lane, acc, visits,
                      work);
         return true;
     }
     if (warp_count<WPL>(X) > 32) return false;
     uint32_t myrow;
     const int n = compress<WPL>(rows, RS, X, list, S.srow, lane, myrow);
-    orient_small(S.srow, n == 32 ? FULL : ((1u << n) - 1u), s, last, S.sstk, lane, acc, visits,
+    orient_small<G>(S.srow, n == 32 ? FULL : ((1u << n) - 1u), s, last, S.sstk, lane, acc, visits,
                  work);
     return true;
 }
 
-template <int WPL>
+template <int WPL, int G = 32>
 __device__ void orient_subtree(const uint32_t *__restrict__ rows, int RS, int W, int last, int u,
                                const Frames &F, int *list, uint32_t *cbuf, const SmallScratch &SS,
                                ull &acc, ull &visits, ull &work) {
@@ -798,7 +978,8 @@ __device__ void orient_subtree(const uint32_t *__restrict__ rows, int RS, int W,
         return;
     }
     if (!any_set<WPL>(C)) return;
-    if (orient_try_small<WPL>(rows, RS, W, C, 1, last, list, SS, lane, acc, visits, work)) return;
+    if (orient_try_small<WPL, G>(rows, RS, W, C, 1, last, list, SS, lane, acc, visits, work))
+        return;
     if (last == 2) {  // frame 1 is the next-to-last level
         score_pairs<WPL>(rows, RS, W, C, list, cbuf, lane, acc, visits, work);
         return;
@@ -830,7 +1011,8 @@ __device__ void orient_subtree(const uint32_t *__restrict__ rows, int RS, int W,
             X.w[p] = w < W ? (C.w[p] & rv[w]) : 0u;
         }
         if (!any_set<WPL>(X)) continue;
-        if (orient_try_small<WPL>(rows, RS, W, X, s + 1, last, list, SS, lane, acc, visits, work))
+        if (orient_try_small<WPL, G>(rows, RS, W, X, s + 1, last, list, SS, lane, acc, visits,
+                                     work))
             continue;
         if (s + 2 == last) {  // X is the next-to-last frame
             score_pairs<WPL>(rows, RS, W, X, list, cbuf, lane, acc, visits, work);
@@ -982,7 +1164,7 @@ __device__ __forceinline__ void donate_bottom_L(const uint32_t *__restrict__ row
             taken = true;
         } else if (dead) {
             taken = true;
-        } else if (n >= kPushMin && n <= kGItemMax) {
+        } else if (n >= sink.push_min && n <= kGItemMax) {
             taken = push_large<WPL>(sink, X, list, sf + 1, np2, lane);
         }
         if (taken) {

@@ -125,6 +125,8 @@ class RawCount:
     count_ms: float
     word_ops: int = 0        # roofline counters of the counting kernel
     extract_bytes: int = 0
+    group_size: int = 0      # sub-warp group size the orientation warp tier ran with
+    launches: int = 0        # counting-kernel launches
 
     def as_vector(self) -> np.ndarray:
         """Flatten for an element-wise u64 all-reduce."""
@@ -141,7 +143,8 @@ class RawCount:
         if self.hist is not None:
             hist = vec[6 + nsm:].reshape(self.hist.shape).copy()
         return RawCount(vec[:4].copy(), int(vec[4]), int(vec[5]), hist, vec[6:6 + nsm].copy(),
-                        self.count_ms, self.word_ops, self.extract_bytes)
+                        self.count_ms, self.word_ops, self.extract_bytes, self.group_size,
+                        self.launches)
 
 
 def device_count_raw(og, cfg: RunConfig, task_lo: int = 0, task_hi: int = -1) -> RawCount:
@@ -163,7 +166,8 @@ def device_count_raw(og, cfg: RunConfig, task_lo: int = 0, task_hi: int = -1) ->
                           hist.size if pivot else 0, _lib._ptr(per_sm), per_sm.size))
     return RawCount(np.array(raw.limbs[:], dtype=np.uint64), int(raw.visits), int(raw.tasks_run),
                     None if hist is None else hist.reshape(dim, dim), per_sm,
-                    float(raw.count_ms), int(raw.word_ops), int(raw.extract_bytes))
+                    float(raw.count_ms), int(raw.word_ops), int(raw.extract_bytes),
+                    int(raw.group_size), int(raw.launches))
 
 
 def used_sms(per_sm, nsm: int) -> list:
@@ -260,7 +264,8 @@ def run_count(g, cfg: RunConfig) -> CountReport:
         dev["count"] = raw.count_ms
         sbytes = scratch_bytes(og, cfg)
         counters = {"word_ops": raw.word_ops, "extract_bytes": raw.extract_bytes,
-                    "kernel_ms": raw.count_ms, "tasks_run": raw.tasks_run}
+                    "kernel_ms": raw.count_ms, "tasks_run": raw.tasks_run,
+                    "group_size": raw.group_size, "launches": raw.launches}
     count_ms = (time.perf_counter() - t1) * 1000.0
     return CountReport(n=g.n, m=g.m, d_max_undirected=g.max_degree(), d_max=og.d_max, config=cfg,
                        count=count, counts=counts, orient_ms=orient_ms, count_ms=count_ms,

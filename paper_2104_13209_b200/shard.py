@@ -41,14 +41,33 @@ def balanced_ranges(costs: np.ndarray, world: int) -> list[tuple[int, int]]:
     return [(int(cuts[i]), int(cuts[i + 1])) for i in range(world)]
 
 
-def task_costs(og, scheme: str) -> np.ndarray:
+def _args(cfg: RunConfig):
+    k = max(cfg.k, 3) if cfg.all_k else cfg.k
+    return _lib.KcCountArgs(k, _lib.ALGO[cfg.algorithm], _lib.SCHEME[cfg.scheme],
+                            1 if cfg.all_k else 0, int(cfg.group_size), 0, 0, -1)
+
+
+def task_costs(og, cfg: RunConfig) -> np.ndarray:
+    """Per-task cost estimate in make_tasks order (kc_task_costs, on the device)."""
     L = _lib.load()
     h = og.ensure_on_device()
     n = ctypes.c_int64()
-    _lib.check(L.kc_num_tasks(h, _lib.SCHEME[scheme], ctypes.byref(n)))
+    _lib.check(L.kc_num_tasks(h, _lib.SCHEME[cfg.scheme], ctypes.byref(n)))
     costs = np.zeros(max(n.value, 1), dtype=np.int64)
-    _lib.check(L.kc_task_costs(h, _lib.SCHEME[scheme], _lib._ptr(costs), n.value))
+    a = _args(cfg)
+    _lib.check(L.kc_task_costs(h, ctypes.byref(a), _lib._ptr(costs), n.value))
     return costs[:n.value]
+
+
+def shard_ranges(og, cfg: RunConfig, world: int) -> list[tuple[int, int]]:
+    """balanced_ranges over kc_task_costs, computed on the device: only the
+    world + 1 cuts cross to the host (kc_shard_ranges)."""
+    L = _lib.load()
+    h = og.ensure_on_device()
+    cuts = np.zeros(world + 1, dtype=np.int64)
+    a = _args(cfg)
+    _lib.check(L.kc_shard_ranges(h, ctypes.byref(a), int(world), _lib._ptr(cuts)))
+    return [(int(cuts[i]), int(cuts[i + 1])) for i in range(world)]
 
 
 def spread_per_rank(raw: RawCount, rank: int, world: int) -> RawCount:
@@ -59,7 +78,7 @@ def spread_per_rank(raw: RawCount, rank: int, world: int) -> RawCount:
     wide = np.zeros(world * per.size, dtype=np.uint64)
     wide[rank * per.size:(rank + 1) * per.size] = per
     return RawCount(raw.limbs, raw.visits, raw.tasks_run, raw.hist, wide, raw.count_ms,
-                    raw.word_ops, raw.extract_bytes)
+                    raw.word_ops, raw.extract_bytes, raw.group_size, raw.launches)
 
 
 def per_rank_sms(wide, world: int, nsm: int) -> list:
@@ -103,7 +122,7 @@ def run_count_sharded(g, cfg: RunConfig, rank: int, world: int, group=None,
     orient_ms = (time.perf_counter() - t0) * 1000.0
     t1 = time.perf_counter()
     if ranges is None:
-        ranges = balanced_ranges(task_costs(og, cfg.scheme), world)
+        ranges = shard_ranges(og, cfg, world)
     lo, hi = ranges[rank]
     raw = device_count_raw(og, cfg, lo, hi)
     counters = {"word_ops": raw.word_ops, "extract_bytes": raw.extract_bytes,

@@ -34,7 +34,7 @@ def test_library_exports_every_symbol(lib):
     L = lib.load()
     for name in header_symbols():
         assert hasattr(L, name), name
-    assert L.kc_abi_version() == 1
+    assert L.kc_abi_version() == 2
 
 
 def test_sm100a_cubin_inside(lib):
