@@ -500,13 +500,15 @@ class CpuBaseline:
     tasks, min(d+(u), d+(v)) for edge tasks) and every `step`-th one is taken
     (a systematic sample across all strata, heavy tasks included); `step` is
     calibrated once so a sample costs ~target_s of wall time.
-    measure(): the pool runs the sample with its atomic cursor, heaviest task
-    first (LPT order: balanced); the whole-graph estimate is
-        wall = orient_s + step * sample wall time
-    (each sampled task stands for `step` tasks of its stratum) and value =
-    exact count / wall.  The per-thread CPU-time projection is reported next
-    to it, and the committed whole-graph oracle run of the same workload
-    (tests/golden/scale.json: count, wall, cores, CPU model) as `full_run`."""
+    measure(): the pool runs the sample (heaviest task first) and reports
+    every thread's CPU time; the whole-graph estimate is the ratio estimator
+        wall = orient_s + (sample thread-CPU s) * (full count / sample count) / cores
+    i.e. the sample's cliques per core-second, with the full run's work queue
+    keeping every core busy (thread-CPU time is immune to the sample's tail
+    imbalance; the full run has 10^5+ tasks).  value = exact count / wall.
+    The stratum-scaled projection is reported next to it, and the committed
+    whole-graph oracle run of the same workload (tests/golden/scale.json:
+    count, wall, cores, CPU model) as `full_run`."""
 
     def __init__(self, edges, a, target_s=12.0, workers=None):
         import oracle
@@ -528,10 +530,10 @@ class CpuBaseline:
         self.order = tasks[np.argsort(-proxy, kind="stable")]
         n = max(self.order.size, 1)
         step0 = max(1, n // 256)
-        t0 = time.perf_counter()
-        self._run(step0)
-        w0 = time.perf_counter() - t0
-        self.step = min(n, max(1, int(w0 * step0 / max(target_s, 1e-9))))
+        _, _, b0, _ = self._run(step0)
+        # thread-CPU seconds of the whole graph ~ b0 * step0; a sample of
+        # `target_s` wall on every core takes step = that / (target_s * cores)
+        self.step = min(n, max(1, int(b0 * step0 / max(target_s * self.workers, 1e-9))))
 
     def _run(self, step):
         import oracle
@@ -546,8 +548,12 @@ class CpuBaseline:
         t1 = time.perf_counter()
         c1, v1, b1, n1 = self._run(step)
         sample_wall = time.perf_counter() - t1
-        wall = self.orient_s + sample_wall * step
         count = full_count if full_count is not None else c1 * step
+        # ratio estimator: the sample's cliques per thread-CPU second hold for
+        # the whole graph (cost tracks cliques much more tightly than the
+        # cost proxy does); the full run's pool keeps every core busy
+        busy_full = b1 * (count / c1) if c1 else b1 * step
+        wall = self.orient_s + busy_full / self.workers
         rec = {"value": count / wall if wall > 0 else None, "unit": "k-cliques/s",
                "cores": self.workers, "kind": "port", "cpu_model": _cpu_model(),
                "sample": (f"oracle/kc_oracle.c worker pool on every {step}-th task of "
@@ -555,7 +561,7 @@ class CpuBaseline:
                           f"{100.0 / step:.2f}%; {sample_wall:.1f}s wall, {b1:.1f} thread-CPU s)"
                           f" + full-graph ranking/orientation {self.orient_s:.2f}s"),
                "estimated_full_wall_s": wall, "orient_s_full": self.orient_s,
-               "estimated_full_wall_s_from_thread_cpu": self.orient_s + b1 * step / self.workers,
+               "estimated_full_wall_s_stratum_scaling": self.orient_s + b1 * step / self.workers,
                "sample_count_scaled": str(c1 * step), "sample_visits_scaled": v1 * step,
                "step": step}
         rec.update(full_run_record(self.a))

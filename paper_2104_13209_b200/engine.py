@@ -163,7 +163,7 @@ class BinomialTable:
         if r < 0 or r > n:
             return 0
         if self.too_big[n, r]:
-            raise OverflowError("binomial value exceeds 128 bits")
+            raise OverflowError("binomial value exceeds the 128-bit accumulator")
         return value128(self.lo[n, r], self.hi[n, r])
 
 

@@ -181,7 +181,7 @@ def used_sms(per_sm, nsm: int) -> list:
 def _binom_checked(n: int, r: int) -> int:
     c = math.comb(n, r)
     if c >= _LIMIT_128:
-        raise OverflowError("binomial value exceeds 128 bits")
+        raise OverflowError("binomial value exceeds the 128-bit accumulator")
     return c
 
 
