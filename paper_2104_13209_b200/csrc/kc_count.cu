@@ -505,11 +505,14 @@ constexpr int kAutoGroup = 8;  // orientation sub-warp group size for group_size
 // warp-level bit matrix of the sub-graph induced by the sorted vertices l2g[0..d)
 // (bitgraph.py:89-111: bit j of row i <=> arc l2g[i] -> l2g[j], or either arc)
 __device__ void warp_rows(const CountParams &p, const int32_t *l2g, int d, uint32_t *rows,
-                          bool directed, ull &bytes) {
+                          bool directed, ull &bytes, const kct::SmallScratch &SS) {
     const int lane = threadIdx.x & 31;
     const int W = (d + 31) >> 5, RS = warp_row_stride(W, directed);
     for (int i = lane; i < d * RS; i += 32) rows[i] = 0u;
-    __syncwarp();
+    kct::LocalMap map;
+    map.key = reinterpret_cast<int32_t *>(SS.sstk);
+    map.val = reinterpret_cast<uint8_t *>(SS.sstk + kct::kMapSlots);
+    map.build(l2g, d, lane);  // ends with __syncwarp (rows zeroed too)
     const int32_t lo_id = l2g[0], hi_id = l2g[d - 1];
     for (int i = 0; i < d; ++i) {
         const int32_t gi = l2g[i];
@@ -518,7 +521,7 @@ __device__ void warp_rows(const CountParams &p, const int32_t *l2g, int d, uint3
         for (int64_t e = beg + lane; e < end; e += 32) {
             const int32_t x = p.ocol[e];
             if (x < lo_id || x > hi_id) continue;
-            const int j = smem_find(l2g, d, x);
+            const int j = map.find(x);
             if (j >= 0) {
                 atomicOr(&rows[i * RS + (j >> 5)], 1u << (j & 31));
                 if (!directed) atomicOr(&rows[j * RS + (i >> 5)], 1u << (i & 31));
@@ -530,7 +533,8 @@ __device__ void warp_rows(const CountParams &p, const int32_t *l2g, int d, uint3
 
 // warp-level K4: locals + bit matrix of one task (d <= kWarpD)
 __device__ int warp_build(const CountParams &p, int32_t task, int32_t *l2g, uint32_t *rows,
-                          bool need_rows, bool directed, ull &bytes, int32_t w3 = -1) {
+                          bool need_rows, bool directed, ull &bytes, const kct::SmallScratch &SS,
+                          int32_t w3 = -1) {
     const int lane = threadIdx.x & 31;
     int d;
     if (p.scheme == KC_SCHEME_VERTEX) {
@@ -563,7 +567,7 @@ __device__ int warp_build(const CountParams &p, int32_t task, int32_t *l2g, uint
     __syncwarp();
     if (d > kWarpD) return d;  // caller defers the task to the CTA kernel
     if (!need_rows || d == 0) return d;
-    warp_rows(p, l2g, d, rows, directed, bytes);
+    warp_rows(p, l2g, d, rows, directed, bytes, SS);
     return d;
 }
 
@@ -626,7 +630,7 @@ __global__ void __launch_bounds__(BLOCK) k_count_warp(CountParams p) {
         if (i >= ull(p.n_tasks)) break;
         const int32_t task = p.tasks[i];
         const bool need_rows = MODE == MODE_PIVOT || t >= 2;
-        const int d = warp_build(p, task, l2g, rows, need_rows, MODE == MODE_ORIENT, bytes,
+        const int d = warp_build(p, task, l2g, rows, need_rows, MODE == MODE_ORIENT, bytes, SS,
                                  p.task_w ? p.task_w[i] : -1);
         if (d > D) {  // edge task larger than the warp tier: CTA kernel, next launch
             if (lane == 0) {
@@ -801,7 +805,7 @@ __global__ void __launch_bounds__(BLOCK) k_count_warp(CountParams p) {
                 continue;
             }
             // the subtree of X depends only on the sub-graph induced by X
-            warp_rows(p, l2g, n, rows, false, bytes);
+            warp_rows(p, l2g, n, rows, false, bytes, SS);
             const int W = (n + 31) >> 5, RS = row_stride(W);
             const ull wt0 = work;
             if (W == 1) {

@@ -120,9 +120,63 @@ __device__ __forceinline__ int next_bit(Set<WPL> &R, int lane) {
     return -1;
 }
 
+// position of the k-th (0-based) set bit of x (k < popc(x)); branch-free
+__device__ __forceinline__ int nth_bit(uint32_t x, int k) {
+    int p = 0;
+#pragma unroll
+    for (int w = 16; w; w >>= 1) {
+        const int c = __popc(x & ((1u << w) - 1u));
+        if (k >= c) {
+            k -= c;
+            x >>= w;
+            p += w;
+        }
+    }
+    return p;
+}
+
+// lanes per member so that `cnt` members fill the warp: 32 / pow2ceil(cnt)
+__device__ __forceinline__ int lanes_per_member_log2(int cnt) {
+    return cnt > 16 ? 0 : cnt > 8 ? 1 : cnt > 4 ? 2 : cnt > 2 ? 3 : cnt > 1 ? 4 : 5;
+}
+// bits b of a word with b % 2^lg == sub
+__device__ __forceinline__ uint32_t id_stripe(int lg, int sub) {
+    const uint32_t rep = lg == 5 ? 1u : 0xffffffffu / ((1u << (1 << lg)) - 1u);
+    return rep << sub;
+}
+
+// compact the members of a set of at most four words (C lane-distributed:
+// lane w holds word w) into list[0..n): lane L owns bits [4L, 4L+4), so every
+// lane does at most four iterations (the word-per-lane loop below leaves 28
+// lanes idle for such sets)
+__device__ __forceinline__ int compact4(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
+                                        int *list, int lane) {
+    const int wsel = lane >> 3;
+    const uint32_t word = wsel == 0 ? c0 : wsel == 1 ? c1 : wsel == 2 ? c2 : c3;
+    uint32_t nib = (word >> ((lane & 7) << 2)) & 15u;
+    const int c = __popc(nib);
+    int incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += y;
+    }
+    int off = incl - c;
+    while (nib) {
+        list[off++] = (lane << 2) + __ffs(nib) - 1;
+        nib &= nib - 1u;
+    }
+    const int n = __shfl_sync(FULL, incl, 31);
+    __syncwarp();
+    return n;
+}
+
 // compact the members of C (ascending) into list[0..n); returns n (uniform)
 template <int WPL>
-__device__ __forceinline__ int compact(const Set<WPL> &C, int *list, int lane) {
+__device__ __forceinline__ int compact(const Set<WPL> &C, int *list, int lane, int W = 32 * WPL) {
+    if (WPL == 1 && W <= 4)
+        return compact4(__shfl_sync(FULL, C.w[0], 0), __shfl_sync(FULL, C.w[0], 1),
+                        __shfl_sync(FULL, C.w[0], 2), __shfl_sync(FULL, C.w[0], 3), list, lane);
     int n = 0;
 #pragma unroll
     for (int p = 0; p < WPL; ++p) {
@@ -224,11 +278,59 @@ struct CsaAcc {
     }
 };
 
+// Warp tier, rows of at most four words with a 16-byte stride: the members v
+// of C are spread so that each gets 32 / pow2ceil(#members) lanes (a sub-warp
+// group), and the lanes of a group split v's walk over X_v = C & row v by
+// member id (id stripes); every (v, x) pair costs one LDS.128 and a
+// carry-save add of four words.  Counts and visits are sums, hence unchanged.
+__device__ __forceinline__ void score_pairs4(const uint32_t *__restrict__ rows, const Set<1> &C,
+                                             int *list, int lane, ull &acc, ull &visits,
+                                             ull &work) {
+    const uint32_t c0 = __shfl_sync(FULL, C.w[0], 0), c1 = __shfl_sync(FULL, C.w[0], 1);
+    const uint32_t c2 = __shfl_sync(FULL, C.w[0], 2), c3 = __shfl_sync(FULL, C.w[0], 3);
+    const int n = compact4(c0, c1, c2, c3, list, lane);
+    if (lane == 0) visits += ull(n);
+    unsigned a32 = 0;
+    for (int base = 0; base < n; base += 32) {
+        const int cnt = n - base < 32 ? n - base : 32;
+        const int lg = lanes_per_member_log2(cnt);
+        const int mi = lane >> lg, sub = lane & ((1 << lg) - 1);
+        if (mi >= cnt) continue;
+        const int v = list[base + mi];
+        const uint4 rv = *reinterpret_cast<const uint4 *>(rows + (v << 2));
+        const uint32_t cm0 = c0 & rv.x, cm1 = c1 & rv.y, cm2 = c2 & rv.z, cm3 = c3 & rv.w;
+        if (sub == 0) {
+            const ull xs = ull(__popc(cm0) + __popc(cm1) + __popc(cm2) + __popc(cm3));
+            visits += xs;
+            work += 1 + xs;
+        }
+        const uint32_t st = id_stripe(lg, sub);
+        CsaAcc h;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+            uint32_t m = (w == 0 ? cm0 : w == 1 ? cm1 : w == 2 ? cm2 : cm3) & st;
+            while (m) {
+                const int b = 31 - __clz(m);
+                m ^= 1u << b;
+                const uint4 r = *reinterpret_cast<const uint4 *>(rows + (((w << 5) + b) << 2));
+                h.add4(cm0 & r.x, cm1 & r.y, cm2 & r.z, cm3 & r.w);
+            }
+        }
+        a32 += h.total();
+    }
+    acc += a32;
+    __syncwarp();
+}
+
 template <int WPL>
 __device__ __forceinline__ void score_pairs(const uint32_t *__restrict__ rows, int RS, int W,
                                             const Set<WPL> &C, int *list, uint32_t *cbuf,
                                             int lane, ull &acc, ull &visits, ull &work) {
-    const int n = compact<WPL>(C, list, lane);
+    if (WPL == 1 && W >= 2 && W <= 4 && RS == 4) {
+        score_pairs4(rows, reinterpret_cast<const Set<1> &>(C), list, lane, acc, visits, work);
+        return;
+    }
+    const int n = compact<WPL>(C, list, lane, W);
     store_set<WPL>(cbuf, C, lane);
     __syncwarp();
     visits += ull(popc_set<WPL>(C));
@@ -338,7 +440,7 @@ template <int WPL>
 __device__ __forceinline__ int select_pivot(const uint32_t *__restrict__ rows, int RS,
                                             const Set<WPL> &C, int *list, int lane, ull &work,
                                             int W) {
-    const int n = compact<WPL>(C, list, lane);
+    const int n = compact<WPL>(C, list, lane, W);
     ull best = 0;
     for (int base = 0; base < n; base += 32) {
         const int i = base + lane;
@@ -377,8 +479,8 @@ __device__ __forceinline__ int warp_count(const Set<WPL> &X) {
 template <int WPL>
 __device__ __forceinline__ int compress(const uint32_t *__restrict__ rows, int RS,
                                         const Set<WPL> &X, int *list, uint32_t *srow, int lane,
-                                        uint32_t &myrow) {
-    const int n = compact<WPL>(X, list, lane);
+                                        uint32_t &myrow, int W = 32 * WPL) {
+    const int n = compact<WPL>(X, list, lane, W);
     uint32_t r = 0;
     if (lane < n) {
         const uint32_t *rc = rows + list[lane] * RS;
@@ -562,12 +664,20 @@ __device__ __forceinline__ void pair_batch(const uint32_t *__restrict__ rows, co
 // orientation, last two levels over compressed set C (C = frame last-1)
 __device__ __forceinline__ void pairs_small(const uint32_t *srow, uint32_t C, int lane, ull &acc,
                                             ull &visits, ull &work) {
-    if ((C >> lane) & 1u) {
-        const uint32_t cm = C & srow[lane];
-        uint32_t m = cm;
-        const int xs = __popc(m);
-        visits += ull(1 + xs);
-        work += ull(1 + xs);
+    // each member gets 32 / pow2ceil(|C|) lanes; the lanes of a member split
+    // its walk over C & row v by member id
+    const int cnt = __popc(C);
+    const int lg = lanes_per_member_log2(cnt);
+    const int mi = lane >> lg, sub = lane & ((1 << lg) - 1);
+    if (mi < cnt) {
+        const int v = nth_bit(C, mi);
+        const uint32_t cm = C & srow[v];
+        if (sub == 0) {
+            const int xs = __popc(cm);
+            visits += ull(1 + xs);
+            work += ull(1 + xs);
+        }
+        uint32_t m = cm & id_stripe(lg, sub);
         // two members per trip: independent shared loads in flight; the
         // words go through CsaAcc (one POPC per four members)
         CsaAcc h;
@@ -933,13 +1043,47 @@ struct Frames {
     }
 };
 
-// per-warp S-tier scratch: compressed rows and the scalar frame stack
+// per-warp scratch: compressed S-tier rows, and the hash table of the
+// warp-tier sub-graph builder (kMapSlots int32 keys + kMapSlots u8 values)
 struct SmallScratch {
     uint32_t *srow;  // 32 words
-    uint32_t *sstk;  // 5 words per level, kSmallDepth levels
+    uint32_t *sstk;  // kMapWords words: LocalMap storage
 };
-constexpr int kSmallDepth = 36;
-constexpr int kSmallWords = 32 + 5 * kSmallDepth;
+constexpr int kMapSlots = 256;
+constexpr int kMapWords = kMapSlots + kMapSlots / 4;
+constexpr int kSmallWords = 32 + kMapWords;
+
+// global vertex id -> local index of the <= 128 sorted locals of a warp-tier
+// task: open addressing, load factor <= 1/2, so a miss (most out-neighbours
+// are not locals) costs ~2.5 probes instead of a 7-step binary search
+struct LocalMap {
+    int32_t *key;
+    uint8_t *val;
+    __device__ __forceinline__ static uint32_t slot(int32_t x) {
+        return (uint32_t(x) * 0x9E3779B1u) >> 24;  // 8 bits: kMapSlots = 256
+    }
+    // whole warp; l2g[0..d) distinct, d <= kMapSlots / 2
+    __device__ __forceinline__ void build(const int32_t *l2g, int d, int lane) const {
+        for (int i = lane; i < kMapSlots; i += 32) key[i] = -1;
+        __syncwarp();
+        for (int i = lane; i < d; i += 32) {
+            const int32_t x = l2g[i];
+            uint32_t h = slot(x);
+            while (atomicCAS(key + h, -1, x) != -1) h = (h + 1) & (kMapSlots - 1);
+            val[h] = uint8_t(i);
+        }
+        __syncwarp();
+    }
+    __device__ __forceinline__ int find(int32_t x) const {
+        uint32_t h = slot(x);
+        for (;;) {
+            const int32_t k = key[h];
+            if (k == x) return val[h];
+            if (k < 0) return -1;
+            h = (h + 1) & (kMapSlots - 1);
+        }
+    }
+};
 
 // ---------------------------------------------------------------------------
 // orient: one level-1 subtree (engine_orient.py:32-79).  The caller expanded
@@ -960,7 +1104,7 @@ __device__ __forceinline__ bool orient_try_small(const uint32_t *__restrict__ ro
     }
     if (warp_count<WPL>(X) > 32) return false;
     uint32_t myrow;
-    const int n = compress<WPL>(rows, RS, X, list, S.srow, lane, myrow);
+    const int n = compress<WPL>(rows, RS, X, list, S.srow, lane, myrow, W);
     orient_small<G>(S.srow, n == 32 ? FULL : ((1u << n) - 1u), s, last, S.sstk, lane, acc, visits,
                  work);
     return true;
@@ -1051,7 +1195,7 @@ __device__ __forceinline__ bool pivot_try_small(const uint32_t *__restrict__ row
     }
     if (warp_count<WPL>(X) > 32) return false;
     uint32_t myrow;
-    const int n = compress<WPL>(rows, RS, X, list, S.srow, lane, myrow);
+    const int n = compress<WPL>(rows, RS, X, list, S.srow, lane, myrow, W);
     pivot_small(S.srow, myrow, n == 32 ? FULL : ((1u << n) - 1u), s, npv, t, allk, S.sstk, sink,
                 lane, visits, work, list);
     return true;

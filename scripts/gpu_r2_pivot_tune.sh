@@ -4,7 +4,7 @@ mkdir -p gpurun_out
 export PYTHONPATH=$PWD KC_GRAPH_CACHE=/tmp/kc_graphs KC_GQ_DEBUG=1
 J=gpurun_out/r2_pivot_tune.jsonl
 : > $J
-for cfg in "12 256 4" "12 64 4" "12 16 4" "8 16 3" "12 16 2" "24 16 4" "12 4 4"; do
+for cfg in "12 256 4" "12 256 0" "12 64 0" "12 16 0" "8 16 0" "6 16 0" "12 4 0" "24 16 0"; do
   set -- $cfg
   echo "{\"push_min\": $1, \"cooldown\": $2, \"room\": $3}" >> $J
   KC_GQ_PUSHMIN=$1 KC_GQ_COOLDOWN=$2 KC_GQ_ROOM=$3 timeout 300 python scripts/explore.py --workload rmat14 --k 10 --algo pivot --scheme edge vertex --criterion degeneracy --reps 2 >> $J 2>&1
