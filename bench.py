@@ -332,6 +332,14 @@ def run_ours(a):
         side = other_configs(kc, time_steps, local)
 
     roof = roofline(kc, g, cfg, rep, a, local) if rank == 0 else None
+    gold = golden(a.workload, dict(k=a.k, algorithm=a.algo, scheme=a.scheme,
+                                   criterion=a.criterion))
+    full_check = None
+    if gold is not None:
+        full_check = {"count_matches": str(count) == gold["count"],
+                      "visits_match": (None if gold["visits"] is None
+                                       else rep.load.total == gold["visits"]),
+                      "oracle_count": gold["count"], "source": gold["source"]}
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         cpu = cpu_baseline(edges, a, count, target_s=a.cpu_sample_s)
@@ -343,6 +351,7 @@ def run_ours(a):
             "dtype": "u32", "dtype_note": "u32 bitmap words (AND/POPC), u64 count limbs",
             "data": "synthetic (seeded generator)",
             "config": config_dict(a, world), "count": str(count),
+            "full_count_check": full_check,
             "phases_ms": {k: float(np.median(v)) for k, v in phase.items()},
             "d_max": rep.d_max, "degeneracy": rep.degeneracy, "visits": rep.load.total,
             "normalized_max": rep.load.normalized_max, "step_ms": ms,
@@ -357,9 +366,52 @@ def run_ours(a):
         dist.destroy_process_group()
 
 
+def golden(workload, kw):
+    """The reference-generated (tests/golden/medium.json) or full-graph oracle
+    (tests/golden/scale.json) record of this exact run, if one is committed:
+    {"count", "visits", "source"} (all-k: {"counts", "visits", "source"})."""
+    gdir = os.path.join(HERE, "tests", "golden")
+    crit = kw.get("criterion", "degree")
+    try:
+        with open(os.path.join(gdir, "medium.json")) as f:
+            for rec in json.load(f):
+                if rec["name"] != workload:
+                    continue
+                if kw.get("all_k"):
+                    for r in rec.get("all_k", []):
+                        if (r["scheme"], r["criterion"]) == (kw["scheme"], crit):
+                            return {"counts": r["counts"], "visits": r["visits"],
+                                    "source": "tests/golden/medium.json (reference run)"}
+                for r in rec["runs"]:
+                    if (r["k"], r["algorithm"], r["scheme"], r["criterion"]) == (
+                            kw["k"], kw["algorithm"], kw["scheme"], crit):
+                        return {"count": r["count"], "visits": r["visits"],
+                                "source": "tests/golden/medium.json (reference run)"}
+        with open(os.path.join(gdir, "scale.json")) as f:
+            for r in json.load(f):
+                if (r["workload"], r["k"], r["algorithm"], r["scheme"], r["criterion"],
+                        r["all_k"]) == (workload, kw["k"], kw["algorithm"], kw["scheme"], crit,
+                                        bool(kw.get("all_k"))):
+                    return {"count": r["count"], "visits": r["visits"],
+                            "source": "tests/golden/scale.json (full-graph oracle, "
+                                      f"{r['workers']} threads, {r['oracle_count_s']} s)"}
+        # counts do not depend on algorithm, scheme or order: any record of
+        # this workload and k pins the count (visits then unchecked)
+        with open(os.path.join(gdir, "scale.json")) as f:
+            for r in json.load(f):
+                if (r["workload"], r["k"]) == (workload, kw["k"]) and not kw.get("all_k"):
+                    return {"count": r["count"], "visits": None,
+                            "source": "tests/golden/scale.json (full-graph oracle, count only)"}
+    except OSError:
+        pass
+    return None
+
+
 def other_configs(kc, time_steps, local):
     """Side measurements of BASELINE.json configs 0, 2 and 3 (config 1 is the
-    headline; config 4 is the multi-GPU run of this script with --gpus N)."""
+    headline; config 4 is the multi-GPU run of this script with --gpus N),
+    each checked against a committed reference / full-oracle record where one
+    exists (`golden_match`) or against the oracle run here (ER)."""
     import oracle
 
     out = {}
@@ -370,18 +422,26 @@ def other_configs(kc, time_steps, local):
                                                       criterion="degeneracy", all_k=True), False),
         ("planted_allk_pivot_vertex", "planted", dict(k=10, algorithm="pivot", scheme="vertex",
                                                         criterion="degeneracy", all_k=True), False),
-        ("rmat20_k5_orient_vertex", "rmat20", dict(k=5, algorithm="orient", scheme="vertex",
-                                                     criterion="degeneracy"), False),
-        ("rmat20_k5_orient_edge", "rmat20", dict(k=5, algorithm="orient", scheme="edge",
-                                                   criterion="degeneracy"), False),
-        # k = 10 (the metric's third k) where a run takes seconds: RMAT-14
-        ("rmat14_k10_pivot_edge", "rmat14", dict(k=10, algorithm="pivot", scheme="edge",
-                                                   criterion="degeneracy"), "once"),
+        ("rmat18_k4_bulk_order", "rmat18", dict(k=4, algorithm="orient", scheme="vertex",
+                                                 criterion="degeneracy_bulk"), False),
     ]
+    # BASELINE configs[2]: RMAT-20 edge- vs vertex-centric x sub-warp group size
+    for scheme in ("vertex", "edge"):
+        for gs in (32, 8, 1):
+            plan.append((f"rmat20_k5_orient_{scheme}_g{gs}", "rmat20",
+                         dict(k=5, algorithm="orient", scheme=scheme, criterion="degeneracy",
+                              group_size=gs), False))
+    # k = 10 (the metric's third k) where a run takes seconds: RMAT-14
+    for scheme in ("edge", "vertex"):
+        plan.append((f"rmat14_k10_pivot_{scheme}", "rmat14",
+                     dict(k=10, algorithm="pivot", scheme=scheme, criterion="degeneracy"), False))
     graphs = {}
     for name, wl, kw, check in plan:
         try:
             if wl not in graphs:
+                for _, old in graphs.values():
+                    old.free()
+                graphs.clear()
                 e = workload_edges(wl)
                 graphs[wl] = (e, kc.from_edges(e, device=local))
             e, gg = graphs[wl]
@@ -389,16 +449,26 @@ def other_configs(kc, time_steps, local):
             st = lambda gg=gg, c=c: kc.run_count(gg, c)  # noqa: E731
             n_t = 1 if check == "once" else 2
             if check != "once":
-                st()  # warm-up (skipped for the long k=10 run; the library has no JIT)
+                st()  # warm-up (the library has no JIT; pools and caches)
             r, t = time_steps(st, n_t)
             rec = {"config": kw, "count": str(r.count), "ms_per_step": t / n_t,
                    "steps": n_t, "warmup": 0 if check == "once" else 1,
                    "cliques_per_s": r.count * n_t / (t / 1e3) if t else None,
                    "visits": r.load.total, "normalized_max": r.load.normalized_max,
-                   "n": gg.n, "m": gg.m, "d_max": r.d_max}
+                   "n": gg.n, "m": gg.m, "d_max": r.d_max,
+                   "group_size_run": (r.counters or {}).get("group_size")}
             if r.counts:
                 rec["max_k"] = max(r.counts)
                 rec["counts_k10_k30"] = {str(k): str(r.counts.get(k, 0)) for k in (10, 20, 30)}
+            gold = golden(wl, kw)
+            if gold is not None:
+                if "counts" in gold:
+                    ok = {str(k): str(v) for k, v in (r.counts or {}).items()} == gold["counts"]
+                else:
+                    ok = str(r.count) == gold["count"]
+                rec["golden_match"] = bool(ok and (gold["visits"] is None
+                                                   or r.load.total == gold["visits"]))
+                rec["golden_source"] = gold["source"]
             if check is True:  # bit-exact against the CPU oracle on the same input
                 o = oracle.run_count(oracle.from_edges(e), kw["k"], kw["algorithm"], kw["scheme"],
                                      kw["criterion"], workers=os.cpu_count() or 1)

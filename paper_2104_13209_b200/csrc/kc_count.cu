@@ -47,7 +47,14 @@ struct CountParams {
     int t;             // target inside a task
     int all_k;         // pivot all-k
     int split;         // tasks are out-edges of split vertex roots (see kc_do_count)
-    const int32_t *task_w;  // split triples: third vertex w of task (v,u,w), else nullptr
+    const int32_t *task_w;  // split triples: third vertex w of task (v,u,w), else nullptr;
+                            // pivot branch tasks: the root branch v (local index)
+    int branch;             // pivot: tasks are root branches (task, v) of split tasks
+    int roots_only;         // pivot: compute the root frame of each task (split pass)
+    const int32_t *branch_si;   // branch task -> split-task index
+    int32_t *root_piv;          // split task -> root pivot (local index)
+    uint32_t *root_P;           // split task -> root branch set P0 (4 words)
+    int32_t *root_cnt;          // split task -> |P0| (0: task skipped)
     int32_t *overflow;   // warp kernel: edge tasks with more than kWarpD locals
     int32_t *overflow_w;  // and their third vertex (triples)
     ull *overflow_n;
@@ -500,6 +507,7 @@ constexpr int kWarpD = 128;
 constexpr int kGqCap = 4096;  // GPU-wide subtree queue slots (pivot)
 constexpr int kSplitD = 32;  // orientation/vertex: roots above this are split into edge items
 constexpr int kAutoGroup = 8;  // orientation sub-warp group size for group_size = 0
+constexpr int kPivotSplitD = 32;  // pivot: warp-tier tasks above this are split at the root
 
 
 // warp-level bit matrix of the sub-graph induced by the sorted vertices l2g[0..d)
@@ -580,9 +588,11 @@ __global__ void __launch_bounds__(BLOCK) k_count_warp(CountParams p) {
     __shared__ ull s_red[4 * NW];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int hist_cells = MODE == MODE_PIVOT ? kct::kLeafCells : 0;
-    // per warp: l2g[D] rows[D*RSD] list[D] S0[32] P0[32] cbuf[32] small leafhist frames
-    const int per_warp =
-        D + D * RSD + D + 32 * 3 + kct::kSmallWords + hist_cells + p.nsm_frames * p.fw;
+    const int node_words = MODE == MODE_PIVOT ? 2 * kct::kNodeCap : 0;
+    // per warp: l2g[D] rows[D*RSD] list[D] S0[32] P0[32] cbuf[32] small leafhist
+    // node stack frames
+    const int per_warp = D + D * RSD + D + 32 * 3 + kct::kSmallWords + hist_cells + node_words +
+                         p.nsm_frames * p.fw;
     uint32_t *base = reinterpret_cast<uint32_t *>(smem) + warp * per_warp;
     int32_t *l2g = reinterpret_cast<int32_t *>(base);
     uint32_t *rows = base + D;
@@ -594,8 +604,12 @@ __global__ void __launch_bounds__(BLOCK) k_count_warp(CountParams p) {
     SS.srow = cbuf + 32;
     SS.sstk = SS.srow + 32;
     uint32_t *whist = SS.srow + kct::kSmallWords;
+    if (MODE == MODE_PIVOT) {  // per-lane S-tier walks (kct::pivot_lanes)
+        SS.nstk = reinterpret_cast<uint2 *>(whist + hist_cells);
+        SS.ncap = kct::kNodeCap;
+    }
     kct::Frames F;
-    F.sm = whist + hist_cells;
+    F.sm = whist + hist_cells + node_words;
     F.nsm = p.nsm_frames;
     F.fw = p.fw;
     F.gm = p.frames_global ? p.frames_global + (int64_t(blockIdx.x) * NW + warp) * p.frames_slot
@@ -631,7 +645,7 @@ __global__ void __launch_bounds__(BLOCK) k_count_warp(CountParams p) {
         const int32_t task = p.tasks[i];
         const bool need_rows = MODE == MODE_PIVOT || t >= 2;
         const int d = warp_build(p, task, l2g, rows, need_rows, MODE == MODE_ORIENT, bytes, SS,
-                                 p.task_w ? p.task_w[i] : -1);
+                                 p.task_w && !p.branch ? p.task_w[i] : -1);
         if (d > D) {  // edge task larger than the warp tier: CTA kernel, next launch
             if (lane == 0) {
                 const ull at = atomicAdd(p.overflow_n, 1ull);
@@ -648,7 +662,7 @@ __global__ void __launch_bounds__(BLOCK) k_count_warp(CountParams p) {
         } else if (d < t) {
             continue;
         }
-        if (lane == 0) ++tasks;
+        if (lane == 0 && !p.branch) ++tasks;  // a branch task is part of a counted task
         if (t <= 1 && !allk) {
             if (lane == 0) acc += t == 0 ? 1ull : ull(d);
             continue;
@@ -680,9 +694,36 @@ __global__ void __launch_bounds__(BLOCK) k_count_warp(CountParams p) {
                 }
             }
         } else {
-            if (W == 1) {
-                const uint32_t myrow = lane < d ? rows[lane] : 0u;
-                kct::pivot_small(rows, myrow, all, 0, 0, t, allk, SS.sstk, sink, lane, visits,
+            if (p.roots_only || p.branch) {
+                // split pivot task (engine_pivot.py:133-136 root frame): the
+                // roots pass stores S0's pivot and branch set P0; every
+                // branch v of P0 is then walked as its own task (rebuilding
+                // the task's bit matrix), spreading big trees over the GPU
+                kct::Set<WPL> A;
+                {
+                    const int lo = lane << 5;
+                    A.w[0] = lo >= d ? 0u : (lo + 32 <= d ? kct::FULL : ((1u << (d - lo)) - 1u));
+                }
+                if (p.roots_only) {
+                    const int piv0 = kct::select_pivot<WPL>(rows, RS, A, list, lane, work, W);
+                    const uint32_t rp = lane < W ? rows[piv0 * RS + lane] : 0u;
+                    const uint32_t P = A.w[0] & ~rp;
+                    if (lane < 4) p.root_P[4 * i + lane] = P;
+                    const int c = kct::warp_count<WPL>(kct::Set<WPL>{{P}});
+                    if (lane == 0) {
+                        p.root_piv[i] = piv0;
+                        p.root_cnt[i] = c;
+                    }
+                } else {
+                    const int si = p.branch_si[i];
+                    S0[lane] = A.w[0];
+                    P0[lane] = lane < 4 ? p.root_P[4 * si + lane] : 0u;
+                    __syncwarp();
+                    kct::pivot_subtree<WPL>(rows, RS, W, t, allk, p.task_w[i], p.root_piv[si], S0,
+                                            P0, F, list, SS, sink, visits, work);
+                }
+            } else if (W == 1) {
+                kct::pivot_lanes(rows, all, 0, 0, t, allk, SS.nstk, SS.ncap, sink, lane, visits,
                                  work);
             } else {
                 // root frame: S0 = all locals, pivot = argmax |row c| (lowest id on ties)
@@ -792,11 +833,8 @@ __global__ void __launch_bounds__(BLOCK) k_count_warp(CountParams p) {
                 q.release();
             }
             if (kind == 1u) {  // compressed S-tier subtree: no rebuild
-                const uint32_t myrow = SS.srow[lane];
-                const ull wt1 = work;
-                kct::pivot_small(SS.srow, myrow, h0, s0, npv, t, allk, SS.sstk, sink, lane, visits,
-                                 work);
-                (void)wt1;
+                kct::pivot_lanes(SS.srow, h0, s0, npv, t, allk, SS.nstk, SS.ncap, sink, lane,
+                                 visits, work);
                 if (lane == 0) {
                     atomicAdd(q.ctl + 2, 1);
                     atomicSub(q.ctl + 3, 1);
@@ -810,8 +848,7 @@ __global__ void __launch_bounds__(BLOCK) k_count_warp(CountParams p) {
             const ull wt0 = work;
             if (W == 1) {
                 const uint32_t all = n >= 32 ? kct::FULL : ((1u << n) - 1u);
-                const uint32_t myrow = lane < n ? rows[lane] : 0u;
-                kct::pivot_small(rows, myrow, all, s0, npv, t, allk, SS.sstk, sink, lane, visits,
+                kct::pivot_lanes(rows, all, s0, npv, t, allk, SS.nstk, SS.ncap, sink, lane, visits,
                                  work);
             } else {
                 kct::Set<WPL> A;
@@ -949,6 +986,30 @@ __global__ void k_make_triples(const int64_t *__restrict__ orow, const int32_t *
     }
 }
 
+// branch tasks of the split pivot tasks: (task, v) for every v of P0, in
+// task order (the biggest tasks' branches first)
+__global__ void k_branch_list(const int32_t *__restrict__ cnt, const int32_t *__restrict__ off,
+                              const uint32_t *__restrict__ rootP, int64_t n,
+                              const int32_t *__restrict__ tasks, int32_t *__restrict__ btask,
+                              int32_t *__restrict__ bv, int32_t *__restrict__ bsi) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        if (!cnt[i]) continue;
+        int at = off[i];
+        for (int w = 0; w < 4; ++w) {
+            uint32_t m = rootP[4 * i + w];
+            while (m) {
+                const int b = __ffs(m) - 1;
+                m &= m - 1u;
+                btask[at] = tasks[i];
+                bv[at] = (w << 5) + b;
+                bsi[at] = int32_t(i);
+                ++at;
+            }
+        }
+    }
+}
+
 __global__ void k_mark_roots(const int32_t *__restrict__ roots, int64_t n,
                              uint8_t *__restrict__ vsel) {
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
@@ -982,6 +1043,8 @@ struct DevBuf {
     cudaStream_t s = nullptr;
     DevBuf() = default;
     explicit DevBuf(size_t bytes) : s(tl_stream) { p = kc_alloc<uint8_t>(bytes, s); }
+    // stream-ordered on `st`: the buffer of a kernel launched on st (freed on st)
+    DevBuf(size_t bytes, cudaStream_t st) : s(st) { p = kc_alloc<uint8_t>(bytes, s); }
     ~DevBuf() { kc_free(p, s); }
     template <typename T>
     T *as() const {
@@ -995,7 +1058,9 @@ struct DevBuf {
 // order with enough locals, sorted by descending cost (largest first keeps the
 // persistent queue balanced).  Returns the count.
 int64_t build_tasks(kc_graph *g, int scheme, int64_t lo, int64_t hi, int min_d, DevBuf &out,
-                    uint32_t big_thr, int64_t *n_big, const uint8_t *vsel = nullptr) {
+                    uint32_t big_thr, int64_t *n_big, const uint8_t *vsel = nullptr,
+                    uint32_t mid_thr = 0, int64_t *n_mid = nullptr) {
+    if (n_mid) *n_mid = 0;
     const int64_t N = scheme == KC_SCHEME_EDGE ? g->m_dir : g->n;
     *n_big = 0;
     if (N == 0) return 0;
@@ -1046,11 +1111,15 @@ int64_t build_tasks(kc_graph *g, int scheme, int64_t lo, int64_t hi, int min_d, 
             out.as<int32_t>(), int(n_sel), 0, 32, g->stream));
         k_split_point<<<1, 1, 0, g->stream>>>(key.as<uint32_t>(), n_sel, big_thr,
                                               cnt.as<int32_t>() + 1);
-        int32_t nb = 0;
-        KC_CUDA(cudaMemcpyAsync(&nb, cnt.as<int32_t>() + 1, 4, cudaMemcpyDeviceToHost,
+        if (n_mid)
+            k_split_point<<<1, 1, 0, g->stream>>>(key.as<uint32_t>(), n_sel, mid_thr,
+                                                  cnt.as<int32_t>() + 2);
+        int32_t nb[2] = {0, 0};
+        KC_CUDA(cudaMemcpyAsync(nb, cnt.as<int32_t>() + 1, 8, cudaMemcpyDeviceToHost,
                                 g->stream));
         KC_CUDA(cudaStreamSynchronize(g->stream));
-        *n_big = nb;
+        *n_big = nb[0];
+        if (n_mid) *n_mid = nb[1];
     }
     return n_sel;
 }
@@ -1061,7 +1130,7 @@ constexpr int kSmidSlots = 1024;  // %smid can exceed the SM count
 // limbs, [5] visits, [6] tasks run, [7] warp-tier counter, [8, 8+kSmidSlots)
 // visits per SM, then word_ops, extract bytes, four more task counters and
 // the overflow count, then the subtree queue's control words (8 ints)
-constexpr int kOutGq = 8 + kSmidSlots + 8;
+constexpr int kOutGq = 8 + kSmidSlots + 12;
 constexpr int kOutWords = kOutGq + 4;
 constexpr int kSmemMax = 220 * 1024;
 constexpr int kSmemTarget = 100 * 1024;  // aim for >= 2 resident CTAs per SM
@@ -1075,18 +1144,9 @@ int frames_needed(int mode, int t, int dcap) {
 
 typedef std::vector<std::unique_ptr<DevBuf>> Keep;
 
-// DevBuf memory is stream-ordered on the graph stream; a kernel launched on
-// another stream (the aux stream of the concurrent warp tier) must not start
-// before those allocations -- the pool may hand it blocks the graph stream
-// freed a moment ago while its kernels still read them
-void order_after_allocs(kc_graph *g, cudaStream_t stream) {
-    if (stream == g->stream) return;
-    cudaEvent_t ev;
-    KC_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-    KC_CUDA(cudaEventRecord(ev, g->stream));
-    KC_CUDA(cudaStreamWaitEvent(stream, ev, 0));
-    KC_CUDA(cudaEventDestroy(ev));
-}
+// Buffers of a kernel are allocated stream-ordered on the stream it is
+// launched on (DevBuf(bytes, stream)), so a kernel on the aux stream never
+// waits for, nor races with, the graph stream's allocations and frees.
 
 template <int MODE, int WPL>
 void launch_wpl(kc_graph *g, CountParams &p, int grid_override, Keep &keep,
@@ -1127,17 +1187,16 @@ void launch_wpl(kc_graph *g, CountParams &p, int grid_override, Keep &keep,
     if (grid < 1) grid = 1;
     if (!p.rows_in_smem) {
         p.rows_slot = int64_t(rows_words);
-        keep.emplace_back(new DevBuf(4 * rows_words * size_t(grid)));
+        keep.emplace_back(new DevBuf(4 * rows_words * size_t(grid), stream));
         p.rows_global = keep.back()->as<uint32_t>();
     }
     p.frames_global = nullptr;
     p.frames_slot = 0;
     if (MODE != MODE_EXTRACT && need > nsm) {
         p.frames_slot = int64_t(need - nsm) * p.fw;
-        keep.emplace_back(new DevBuf(4 * size_t(p.frames_slot) * size_t(grid) * NW));
+        keep.emplace_back(new DevBuf(4 * size_t(p.frames_slot) * size_t(grid) * NW, stream));
         p.frames_global = keep.back()->as<uint32_t>();
     }
-    order_after_allocs(g, stream);
     kern<<<grid, kBlock, smem, stream>>>(p);
     KC_CUDA(cudaGetLastError());
     ++tl_launches;
@@ -1151,7 +1210,8 @@ void launch_warp(kc_graph *g, CountParams &p, Keep &keep, cudaStream_t stream) {
     const size_t hist_words = MODE == MODE_PIVOT ? kct::kLeafCells : 0;
     p.fw = MODE == MODE_PIVOT ? 64 + 4 : 32 + 4;
     const int need = std::max(1, std::min(frames_needed(MODE, p.t, D), D + 2));
-    const size_t fixed = size_t(D) + D * RSD + D + 96 + kct::kSmallWords + hist_words;
+    const size_t fixed = size_t(D) + D * RSD + D + 96 + kct::kSmallWords + hist_words +
+                         (MODE == MODE_PIVOT ? 2 * kct::kNodeCap : 0);
     int nsm = std::min(need, 8);
     p.nsm_frames = nsm;
     const size_t smem = 4 * size_t(NW) * (fixed + size_t(nsm) * p.fw) + 64;
@@ -1181,10 +1241,9 @@ void launch_warp(kc_graph *g, CountParams &p, Keep &keep, cudaStream_t stream) {
     p.frames_slot = 0;
     if (need > nsm) {
         p.frames_slot = int64_t(need - nsm) * p.fw;
-        keep.emplace_back(new DevBuf(4 * size_t(p.frames_slot) * size_t(grid) * NW));
+        keep.emplace_back(new DevBuf(4 * size_t(p.frames_slot) * size_t(grid) * NW, stream));
         p.frames_global = keep.back()->as<uint32_t>();
     }
-    order_after_allocs(g, stream);
     kern<<<grid, kBlock, smem, stream>>>(p);
     KC_CUDA(cudaGetLastError());
     ++tl_launches;
@@ -1257,9 +1316,18 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
         KC_CUDA(cudaGetLastError());
     }
     DevBuf tasks;
-    int64_t n_big = 0;
+    int64_t n_big = 0, n_mid = 0;
+    // pivot: warp-tier tasks above kPivotSplitD locals are split at the root
+    static const int pivot_split_d = [] {
+        const char *e = getenv("KC_PIVOT_SPLIT");
+        return e && *e ? atoi(e) : kPivotSplitD;  // 0 / >= 128: off
+    }();
+    const bool psplit = pivot && (a->all_k || t >= 2) && pivot_split_d > 0 &&
+                        pivot_split_d < kWarpD;
     const int64_t n_tasks =
-        build_tasks(g, a->scheme, lo, hi, min_d, tasks, split ? kSplitD : kWarpD, &n_big);
+        build_tasks(g, a->scheme, lo, hi, min_d, tasks, split ? kSplitD : kWarpD, &n_big, nullptr,
+                    uint32_t(pivot_split_d), psplit ? &n_mid : nullptr);
+    const int64_t n_split = psplit ? std::max<int64_t>(n_mid - n_big, 0) : 0;
     DevBuf items;
     int64_t n_items = 0, n_items_big = 0;
     if (split && n_big > 0) {
@@ -1425,10 +1493,66 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
             if (pivot) launch<MODE_PIVOT>(g, b, 0, keep, g->stream);
             else launch<MODE_ORIENT>(g, b, 0, keep, g->stream);
         }
-        if (n_tasks - n_big > 0) {
+        int64_t first = n_big;  // warp-tier tasks not yet launched
+        if (pivot && n_split > 0) {
+            // pivot root split: the warp-tier tasks with more than
+            // kPivotSplitD locals become one task per root branch
+            keep.emplace_back(new DevBuf(4 * size_t(n_split), g->aux));
+            int32_t *root_piv = keep.back()->as<int32_t>();
+            keep.emplace_back(new DevBuf(16 * size_t(n_split), g->aux));
+            uint32_t *root_P = keep.back()->as<uint32_t>();
+            keep.emplace_back(new DevBuf(4 * size_t(n_split), g->aux));
+            int32_t *root_cnt = keep.back()->as<int32_t>();
+            keep.emplace_back(new DevBuf(4 * size_t(n_split), g->aux));
+            int32_t *boff = keep.back()->as<int32_t>();
+            KC_CUDA(cudaMemsetAsync(root_cnt, 0, 4 * size_t(n_split), g->aux));
+            CountParams r = p;
+            r.tasks = tasks.as<int32_t>() + n_big;
+            r.n_tasks = n_split;
+            r.roots_only = 1;
+            r.use_gq = 0;
+            r.root_piv = root_piv;
+            r.root_P = root_P;
+            r.root_cnt = root_cnt;
+            r.task_counter = o + 8 + kSmidSlots + 7;
+            launch_warp<MODE_PIVOT>(g, r, keep, g->aux);
+            size_t bytes = 0;
+            KC_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, root_cnt, boff, int(n_split),
+                                                  g->aux));
+            keep.emplace_back(new DevBuf(bytes > 0 ? bytes : 1, g->aux));
+            void *tmp = keep.back()->p;
+            KC_CUDA(cub::DeviceScan::ExclusiveSum(tmp, bytes, root_cnt, boff, int(n_split),
+                                                  g->aux));
+            int32_t hl[2] = {0, 0};
+            KC_CUDA(cudaMemcpyAsync(&hl[0], boff + n_split - 1, 4, cudaMemcpyDeviceToHost, g->aux));
+            KC_CUDA(cudaMemcpyAsync(&hl[1], root_cnt + n_split - 1, 4, cudaMemcpyDeviceToHost,
+                                    g->aux));
+            KC_CUDA(cudaStreamSynchronize(g->aux));
+            const int64_t nb = int64_t(hl[0]) + hl[1];
+            if (nb > 0) {
+                keep.emplace_back(new DevBuf(12 * size_t(nb), g->aux));
+                int32_t *bt = keep.back()->as<int32_t>();
+                k_branch_list<<<grid_1d(n_split, g->num_sms), 256, 0, g->aux>>>(
+                    root_cnt, boff, root_P, n_split, tasks.as<int32_t>() + n_big, bt, bt + nb,
+                    bt + 2 * nb);
+                KC_CUDA(cudaGetLastError());
+                CountParams b = p;
+                b.branch = 1;
+                b.tasks = bt;
+                b.task_w = bt + nb;
+                b.branch_si = bt + 2 * nb;
+                b.root_piv = root_piv;
+                b.root_P = root_P;
+                b.n_tasks = nb;
+                b.task_counter = o + 8 + kSmidSlots + 8;
+                launch_warp<MODE_PIVOT>(g, b, keep, g->aux);
+            }
+            first = n_big + n_split;
+        }
+        if (n_tasks - first > 0) {
             CountParams q = p;
-            q.tasks = tasks.as<int32_t>() + n_big;
-            q.n_tasks = n_tasks - n_big;
+            q.tasks = tasks.as<int32_t>() + first;
+            q.n_tasks = n_tasks - first;
             q.task_counter = o + 7;
             if (pivot) launch_warp<MODE_PIVOT>(g, q, keep, g->aux);
             else launch_warp<MODE_ORIENT>(g, q, keep, g->aux);

@@ -208,28 +208,43 @@ __global__ void k_comp_small(const int32_t *__restrict__ cverts, const int32_t *
     }
 }
 
-// One big component per CTA (one warp): residual degrees dg[s], the minimum
-// key of every 32-vertex block (bmin) and of every 32-block super-block
-// (smin).  A decrement only lowers keys (atomicMin up the two levels); a pop
-// recomputes its own block and super-block.  Key = (min(deg, k+1) << lbits) |
-// local index (local order = id order).
-template <bool SMEM>
+// internal-row bounds of every vertex, in component order (one dependent
+// load per heap step instead of cverts -> irow)
+__global__ void k_local_rows(const int32_t *__restrict__ cverts, const int64_t *__restrict__ irow,
+                             int64_t n, int2 *__restrict__ lrow) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        const int32_t v = cverts[i];
+        lrow[i] = make_int2(int32_t(irow[v]), int32_t(irow[v + 1]));
+    }
+}
+
+// One big component per CTA (one warp): residual degrees dg[s] (16-bit in
+// shared memory when the component's degrees fit, else 32-bit, in shared or
+// global memory), the minimum key of every 32-vertex block (bmin) and of
+// every 32-block super-block (smin), both in shared memory.  A decrement only
+// lowers keys (atomicMin up the two levels); a pop recomputes its own block
+// and super-block.  Key = (min(deg, k+1) << lbits) | local index (local order
+// = id order).
+template <typename DT, bool SMEM>
 __global__ void __launch_bounds__(32)
     k_comp_big(const int32_t *__restrict__ big, const int32_t *__restrict__ cverts,
                const int32_t *__restrict__ cstart, int64_t n_comp, int64_t n,
                const int32_t *__restrict__ core, const int32_t *__restrict__ deg0,
-               const int64_t *__restrict__ irow, const int32_t *__restrict__ iloc,
+               const int2 *__restrict__ lrow, const int32_t *__restrict__ iloc,
                int32_t *__restrict__ pos, ull *__restrict__ ekey, uint32_t *gscratch,
                int64_t gslot, int32_t *__restrict__ err) {
     extern __shared__ uint32_t sm[];
+    constexpr DT kDeadT = DT(~DT(0));
     const int lane = threadIdx.x;
     const int64_t c = big[blockIdx.x];
     const int32_t b0 = cstart[c];
     const int32_t s = int32_t((c + 1 < n_comp ? cstart[c + 1] : n) - b0);
     const int nb = (s + 31) >> 5, ns = (nb + 31) >> 5;
-    uint32_t *dg = SMEM ? sm : gscratch + int64_t(blockIdx.x) * gslot;
-    uint32_t *bmin = dg + ((s + 3) & ~3);
+    uint32_t *bmin = sm;
     uint32_t *smin = bmin + ((nb + 3) & ~3);
+    DT *dg = SMEM ? reinterpret_cast<DT *>(smin + ((ns + 3) & ~3))
+                  : reinterpret_cast<DT *>(gscratch + int64_t(blockIdx.x) * gslot);
     int lbits = 0;
     while ((1 << lbits) < s) ++lbits;
     const int32_t k = core[cverts[b0]];
@@ -237,10 +252,10 @@ __global__ void __launch_bounds__(32)
     if (lane == 0 && (uint64_t(cap) << lbits) >= 0xffffffffull) atomicExch(err, 2);
     auto key_of = [&](int i) -> uint32_t {
         if (i >= s) return kDead;
-        const uint32_t d = dg[i];
-        return d == kDead ? kDead : ((d < cap ? d : cap) << lbits) | uint32_t(i);
+        const DT d = dg[i];
+        return d == kDeadT ? kDead : ((uint32_t(d) < cap ? uint32_t(d) : cap) << lbits) | uint32_t(i);
     };
-    for (int i = lane; i < s; i += 32) dg[i] = uint32_t(deg0[cverts[b0 + i]]);
+    for (int i = lane; i < s; i += 32) dg[i] = DT(deg0[cverts[b0 + i]]);
     __syncwarp();
     for (int bb = 0; bb < nb; ++bb) {
         const uint32_t m = __reduce_min_sync(FULL, key_of(bb * 32 + lane));
@@ -260,22 +275,24 @@ __global__ void __launch_bounds__(32)
         m = __reduce_min_sync(FULL, m);
         const int p = int(m & lmask);
         const uint32_t dp = m >> lbits;
-        const int32_t vp = cverts[b0 + p];
+        const int32_t vp = cverts[b0 + p];  // only for the outputs below
         if (lane == 0) {
             if (dp > uint32_t(k)) atomicExch(err, 1);
             const ull ek = (ull(dp) << 32) | ull(uint32_t(vp));
             emax = ek > emax ? ek : emax;
             pos[vp] = step;
             ekey[vp] = emax;
-            dg[p] = kDead;
+            dg[p] = kDeadT;
         }
         __syncwarp();
-        for (int64_t e = irow[vp] + lane; e < irow[vp + 1]; e += 32) {
+        const int2 rb = lrow[b0 + p];
+        for (int e = rb.x + lane; e < rb.y; e += 32) {
             const int j = iloc[e];
-            const uint32_t d = dg[j];
-            if (d == kDead) continue;
-            dg[j] = d - 1;  // each neighbour appears once in p's row
-            const uint32_t nk = ((d - 1 < cap ? d - 1 : cap) << lbits) | uint32_t(j);
+            const DT d = dg[j];
+            if (d == kDeadT) continue;
+            dg[j] = DT(d - 1);  // each neighbour appears once in p's row
+            const uint32_t d1 = uint32_t(d) - 1u;
+            const uint32_t nk = ((d1 < cap ? d1 : cap) << lbits) | uint32_t(j);
             atomicMin(bmin + (j >> 5), nk);
             atomicMin(smin + (j >> 10), nk);
         }
@@ -289,6 +306,21 @@ __global__ void __launch_bounds__(32)
         if (lane == 0) smin[ps] = ks;
         __syncwarp();
     }
+}
+
+// max deg0 over vertices of components with more than 32 vertices
+__global__ void k_max_deg_big(const int32_t *__restrict__ cverts, const int32_t *__restrict__ cid1,
+                              const int32_t *__restrict__ cstart, int64_t n_comp, int64_t n,
+                              const int32_t *__restrict__ deg0, int *__restrict__ out) {
+    int local = 0;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t c = cid1[i] - 1;
+        const int64_t sz = (c + 1 < n_comp ? cstart[c + 1] : n) - cstart[c];
+        if (sz > 32) local = max(local, deg0[cverts[i]]);
+    }
+    local = int(__reduce_max_sync(FULL, unsigned(local)));
+    if ((threadIdx.x & 31) == 0 && local) atomicMax(out, local);
 }
 
 // slot of v in (component, pop) order; sort key (core, E)
@@ -418,6 +450,19 @@ void kc_exact_order_from_cores(kc_graph *g, const int32_t *core, int64_t degener
             max_big = std::max(max_big, s);
         }
     }
+    // largest degree in the own core over the big components (16-bit test)
+    int64_t max_deg0_big = 0;
+    if (!hbig.empty()) {
+        Buf dmax(8, st);
+        KC_CUDA(cudaMemsetAsync(dmax.p, 0, 8, st));
+        k_max_deg_big<<<grid_for(n, sms), kT, 0, st>>>(cverts.as<int32_t>(), cid1.as<int32_t>(),
+                                                       cstart.as<int32_t>(), n_comp, n,
+                                                       deg0.as<int32_t>(), dmax.as<int>());
+        int hm = 0;
+        KC_CUDA(cudaMemcpyAsync(&hm, dmax.p, 4, cudaMemcpyDeviceToHost, st));
+        KC_CUDA(cudaStreamSynchronize(st));
+        max_deg0_big = hm;
+    }
     // largest components first (they are the critical path)
     std::sort(hbig.begin(), hbig.end(), [&](int32_t a, int32_t b) {
         return hstart[a + 1] - hstart[a] > hstart[b + 1] - hstart[b];
@@ -433,28 +478,33 @@ void kc_exact_order_from_cores(kc_graph *g, const int32_t *core, int64_t degener
     }
     if (!hbig.empty()) {
         const int64_t nbig = int64_t(hbig.size());
-        Buf dbig(4 * nbig, st);
+        Buf dbig(4 * nbig, st), lrow(8 * n, st);
         KC_CUDA(cudaMemcpyAsync(dbig.p, hbig.data(), 4 * nbig, cudaMemcpyHostToDevice, st));
-        auto words = [](int64_t s) {
-            const int64_t nb = (s + 31) / 32, ns = (nb + 31) / 32;
-            return ((s + 3) & ~int64_t(3)) + ((nb + 3) & ~int64_t(3)) + ns;
+        KC_REQUIRE(m_int < (int64_t(1) << 31), KC_EINVAL, "too many shell-internal arcs");
+        k_local_rows<<<grid_for(n, sms), kT, 0, st>>>(cverts.as<int32_t>(), irow.as<int64_t>(), n,
+                                                     lrow.as<int2>());
+        const int64_t nb = (max_big + 31) / 32, ns = (nb + 31) / 32;
+        const int64_t lvl_words = ((nb + 3) & ~int64_t(3)) + ((ns + 3) & ~int64_t(3));
+        constexpr int64_t kSmemBytes = 200 * 1024;
+        // 16-bit residual degrees when every degree of the big components fits
+        const bool narrow = max_deg0_big < 0xffff;
+        const int64_t dg_bytes = (narrow ? 2 : 4) * ((max_big + 3) & ~int64_t(3));
+        const int64_t smem_all = 4 * lvl_words + dg_bytes;
+        auto run = [&](auto kern, size_t smem, uint32_t *gsc, int64_t gslot) {
+            KC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(smem)));
+            kern<<<int(nbig), 32, smem, st>>>(
+                dbig.as<int32_t>(), cverts.as<int32_t>(), cstart.as<int32_t>(), n_comp, n, core,
+                deg0.as<int32_t>(), lrow.as<int2>(), iloc.as<int32_t>(), pos.as<int32_t>(),
+                ekey.as<ull>(), gsc, gslot, err.as<int32_t>());
         };
-        const int64_t wmax = words(max_big);
-        constexpr int64_t kSmemWords = (200 * 1024) / 4;
-        if (wmax <= kSmemWords) {
-            const size_t smem = 4 * size_t(wmax);
-            KC_CUDA(cudaFuncSetAttribute(k_comp_big<true>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-            k_comp_big<true><<<int(nbig), 32, smem, st>>>(
-                dbig.as<int32_t>(), cverts.as<int32_t>(), cstart.as<int32_t>(), n_comp, n, core,
-                deg0.as<int32_t>(), irow.as<int64_t>(), iloc.as<int32_t>(), pos.as<int32_t>(),
-                ekey.as<ull>(), nullptr, 0, err.as<int32_t>());
+        if (smem_all <= kSmemBytes) {
+            if (narrow) run(k_comp_big<uint16_t, true>, size_t(smem_all), nullptr, 0);
+            else run(k_comp_big<uint32_t, true>, size_t(smem_all), nullptr, 0);
         } else {
-            Buf gs(4 * size_t(wmax) * size_t(nbig), st);
-            k_comp_big<false><<<int(nbig), 32, 0, st>>>(
-                dbig.as<int32_t>(), cverts.as<int32_t>(), cstart.as<int32_t>(), n_comp, n, core,
-                deg0.as<int32_t>(), irow.as<int64_t>(), iloc.as<int32_t>(), pos.as<int32_t>(),
-                ekey.as<ull>(), gs.as<uint32_t>(), wmax, err.as<int32_t>());
+            const int64_t gslot = (max_big + 3) & ~int64_t(3);
+            Buf gs(4 * size_t(gslot) * size_t(nbig), st);
+            run(k_comp_big<uint32_t, false>, size_t(4 * lvl_words), gs.as<uint32_t>(), gslot);
         }
         KC_CUDA(cudaGetLastError());
     }

@@ -908,6 +908,19 @@ struct PivotLeafSink {
             atomicAdd(&g_hist[int64_t(len) * L + np], 1ull);
         }
     }
+    // any lane, concurrently with other lanes (per-lane walks): 32-bit shared
+    // atomics (native), the cell handed to the global u64 histogram at 2^31
+    __device__ __forceinline__ void add_atomic(int len, int np) const {
+        if (len < kLeafHL) {
+            uint32_t *c = &whist[len * (len + 1) / 2 + np];
+            if (atomicAdd(c, 1u) == 0x7fffffffu) {
+                atomicAdd(&g_hist[int64_t(len) * L + np], 0x80000000ull);
+                atomicSub(c, 0x80000000u);
+            }
+        } else {
+            atomicAdd(&g_hist[int64_t(len) * L + np], 1ull);
+        }
+    }
     // whole warp: add the per-warp counters to the global histogram
     __device__ __forceinline__ void flush(int lane) const {
         __syncwarp();
@@ -1030,6 +1043,125 @@ __device__ void pivot_small(const uint32_t *srow, uint32_t myrow, uint32_t C, in
     }
 }
 
+// Per-lane walk of a compressed (<= 32 member) pivot subtree: sub-warp
+// groups of ONE lane (pivoting favours group size 1,
+// PAPER.md:720).  Pending nodes (C, s | npv << 8) sit in a per-warp stack in
+// shared memory; every round each lane pops one node and expands it itself --
+// pivot = argmax |C & row v| over v in C (lowest id on ties,
+// engine_pivot.py:82-101), P = C \ row(pivot), the branches of P under the
+// pruning rule (engine_pivot.py:152-153), child C & row v minus the pruned
+// bits below v (:158-166), leaves binned by (length, pivots) -- and the
+// children are pushed back (counted first, then written at scanned offsets).
+// 32 nodes advance per round instead of one; counts and visits are sums over
+// nodes, so the traversal order does not change them.  When the stack is
+// nearly full a node's subtree is walked by the uniform path instead; while
+// some warp is hungry the bottom (shallowest) node is handed to the GPU-wide
+// queue as a compressed item.
+template <typename Sink>
+__device__ void pivot_lanes(const uint32_t *srow, uint32_t C0, int s0, int npv0, int t, bool allk,
+                            uint2 *nstk, int ncap, const Sink &sink, int lane, ull &visits,
+                            ull &work) {
+    if (lane == 0) nstk[0] = make_uint2(C0, uint32_t(s0) | (uint32_t(npv0) << 16));
+    __syncwarp();
+    int size = 1;  // uniform
+    unsigned vis = 0, wk = 0;
+    const uint32_t myrow = srow[lane];
+    for (;;) {
+        if (size == 0) break;
+        if (sink.gq && size >= 2 && sink.want_push(sink.push_min, 1 << 20, lane)) {
+            const uint2 nb = nstk[0];  // bottom: the shallowest pending node
+            if (__popc(nb.x) >= sink.push_min &&
+                sink.push_compressed(srow, nb.x, int(nb.y & 0xffffu), int(nb.y >> 16), lane)) {
+                __syncwarp();
+                if (lane == 0) nstk[0] = nstk[size - 1];
+                __syncwarp();
+                --size;
+                continue;
+            }
+        }
+        const int free_slots = ncap - size;
+        if (free_slots < 33) {
+            // no room for another round: walk the top node uniformly
+            const uint2 nd = nstk[size - 1];
+            __syncwarp();
+            --size;
+            pivot_small(srow, myrow, nd.x, int(nd.y & 0xffffu), int(nd.y >> 16), t, allk, nullptr,
+                        sink, lane, visits, work);
+            continue;
+        }
+        int k = free_slots / 32;  // each expanded node pushes at most 32 children
+        k = k < 32 ? k : 32;
+        k = k < size ? k : size;
+        uint32_t C = 0;
+        int s = 0, npv = 0;
+        const bool have = lane < k;
+        if (have) {
+            const uint2 nd = nstk[size - 1 - lane];
+            C = nd.x;
+            s = int(nd.y & 0xffffu);
+            npv = int(nd.y >> 16);
+        }
+        size -= k;
+        __syncwarp();
+        int piv = 0, nch = 0;
+        uint32_t P = 0, R = 0;
+        if (have) {
+            // pivot: argmax popc(C & row v), lowest v on ties
+            unsigned best = 0;
+            uint32_t m = C;
+            while (m) {
+                const int v = __ffs(m) - 1;
+                m &= m - 1u;
+                const unsigned key = ((unsigned(__popc(C & srow[v])) + 1u) << 5) | unsigned(31 - v);
+                best = key > best ? key : best;
+            }
+            piv = 31 - int(best & 31u);
+            wk += unsigned(__popc(C));
+            P = C & ~srow[piv];
+            R = (!allk && s + 1 - t > npv) ? (P & (1u << piv)) : P;
+            // branches: visits, leaves, and the number of children to push
+            uint32_t r = R;
+            while (r) {
+                const int v = __ffs(r) - 1;
+                r &= r - 1u;
+                const int np2 = npv + (v == piv ? 1 : 0);
+                if (!allk && s + 1 - t > np2) continue;  // pruned: not a visit
+                ++vis;
+                const uint32_t X = C & srow[v] & ~(P & ((1u << v) - 1u));
+                if (X) {
+                    if (!allk && s + 2 - t > np2 + 1) continue;  // every branch pruned
+                    ++nch;
+                } else if (allk || s + 1 >= t) {
+                    sink.add_atomic(s + 1, np2);
+                }
+            }
+        }
+        int incl = nch;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl += y;
+        }
+        int at = size + incl - nch;
+        size += __shfl_sync(FULL, incl, 31);
+        if (nch) {
+            uint32_t r = R;
+            while (r) {
+                const int v = __ffs(r) - 1;
+                r &= r - 1u;
+                const int np2 = npv + (v == piv ? 1 : 0);
+                if (!allk && s + 1 - t > np2) continue;
+                const uint32_t X = C & srow[v] & ~(P & ((1u << v) - 1u));
+                if (!X || (!allk && s + 2 - t > np2 + 1)) continue;
+                nstk[at++] = make_uint2(X, uint32_t(s + 1) | (uint32_t(np2) << 16));
+            }
+        }
+        __syncwarp();
+    }
+    visits += vis;
+    work += ull(vis) + wk;
+}
+
 // ---------------------------------------------------------------------------
 // frames
 // ---------------------------------------------------------------------------
@@ -1048,7 +1180,10 @@ struct Frames {
 struct SmallScratch {
     uint32_t *srow;  // 32 words
     uint32_t *sstk;  // kMapWords words: LocalMap storage
+    uint2 *nstk = nullptr;  // pivot per-lane node stack (warp tier), nullptr: uniform walks
+    int ncap = 0;
 };
+constexpr int kNodeCap = 512;  // pivot_lanes stack capacity (nodes of 2 words)
 constexpr int kMapSlots = 256;
 constexpr int kMapWords = kMapSlots + kMapSlots / 4;
 constexpr int kSmallWords = 32 + kMapWords;
@@ -1189,6 +1324,10 @@ __device__ __forceinline__ bool pivot_try_small(const uint32_t *__restrict__ row
                                                 ull &work) {
     if (W == 1) {  // rows are already one word: identity relabelling
         const uint32_t c = __shfl_sync(FULL, X.w[0], 0);
+        if (S.nstk && RS == 1) {
+            pivot_lanes(rows, c, s, npv, t, allk, S.nstk, S.ncap, sink, lane, visits, work);
+            return true;
+        }
         const uint32_t myrow = ((c >> lane) & 1u) ? rows[lane * RS] : 0u;
         pivot_small(rows, myrow, c, s, npv, t, allk, S.sstk, sink, lane, visits, work);
         return true;
@@ -1196,6 +1335,11 @@ __device__ __forceinline__ bool pivot_try_small(const uint32_t *__restrict__ row
     if (warp_count<WPL>(X) > 32) return false;
     uint32_t myrow;
     const int n = compress<WPL>(rows, RS, X, list, S.srow, lane, myrow, W);
+    if (S.nstk) {
+        pivot_lanes(S.srow, n == 32 ? FULL : ((1u << n) - 1u), s, npv, t, allk, S.nstk, S.ncap,
+                    sink, lane, visits, work);
+        return true;
+    }
     pivot_small(S.srow, myrow, n == 32 ? FULL : ((1u << n) - 1u), s, npv, t, allk, S.sstk, sink,
                 lane, visits, work, list);
     return true;
