@@ -51,6 +51,12 @@ struct CountParams {
                             // pivot branch tasks: the root branch v (local index)
     int branch;             // pivot: tasks are root branches (task, v) of split tasks
     int roots_only;         // pivot: compute the root frame of each task (split pass)
+    // orientation tasks counted by the pivot engine (CTA tier): t = the task
+    // target T, leaves binned at len + hshift, orientation visits from binom
+    int hybrid, hshift;
+    const ull *binom;
+    int binom_dim;
+    int *hybrid_over;
     const int32_t *branch_si;   // branch task -> split-task index
     int32_t *root_piv;          // split task -> root pivot (local index)
     uint32_t *root_P;           // split task -> root branch set P0 (4 words)
@@ -185,7 +191,36 @@ __device__ int build_task(const CountParams &p, int32_t task, int32_t *l2g, uint
     if (!need_rows || d == 0) return d;
     const int W = (d + 31) >> 5, RS = row_stride(W);
     for (int i = tid; i < d * RS; i += BLOCK) rows[i] = 0u;
+    // orientation: global id -> local index by open addressing over H >= 2d
+    // slots in the (now free) staging area -- a miss costs ~2.5 probes, not a
+    // binary search.  (The pivot engine keeps its per-warp leaf histograms in
+    // that area across tasks, so it searches l2g instead.)
+    int hb = 1;
+    while ((1 << hb) < 2 * d) ++hb;
+    const int H = 1 << hb;
+    int32_t *hkey = scratch;
+    int16_t *hval = reinterpret_cast<int16_t *>(scratch + H);
+    if (directed) {
+        for (int i = tid; i < H; i += BLOCK) hkey[i] = -1;
+        __syncthreads();
+        for (int i = tid; i < d; i += BLOCK) {
+            const int32_t x = l2g[i];
+            uint32_t h = (uint32_t(x) * 0x9E3779B1u) >> (32 - hb);
+            while (atomicCAS(hkey + h, -1, x) != -1) h = (h + 1) & uint32_t(H - 1);
+            hval[h] = int16_t(i);
+        }
+    }
     __syncthreads();
+    auto find = [&](int32_t x) -> int {
+        if (!directed) return smem_find(l2g, d, x);
+        uint32_t h = (uint32_t(x) * 0x9E3779B1u) >> (32 - hb);
+        for (;;) {
+            const int32_t k = hkey[h];
+            if (k == x) return hval[h];
+            if (k < 0) return -1;
+            h = (h + 1) & uint32_t(H - 1);
+        }
+    };
     // bitgraph.py:89-111: bit j of row i <=> l2g[j] in N+(l2g[i]); the scan of
     // each local's out-list replaces the reference's pairwise binary searches
     const int32_t lo_id = l2g[0], hi_id = l2g[d - 1];
@@ -196,7 +231,7 @@ __device__ int build_task(const CountParams &p, int32_t task, int32_t *l2g, uint
         for (int64_t e = beg + lane; e < end; e += 32) {
             const int32_t x = p.ocol[e];
             if (x < lo_id || x > hi_id) continue;
-            const int j = smem_find(l2g, d, x);
+            const int j = find(x);
             if (j >= 0) {
                 atomicOr(&rows[i * RS + (j >> 5)], 1u << (j & 31));
                 if (!directed) atomicOr(&rows[j * RS + (i >> 5)], 1u << (i & 31));
@@ -425,9 +460,19 @@ __global__ void __launch_bounds__(BLOCK) k_count(CountParams p) {
     sink.push_min = p.gq_push_min;
     sink.cooldown = p.gq_cooldown;
     sink.room_min = p.gq_room;
+    __shared__ ull s_hvis[NW];
+    if (MODE == MODE_PIVOT && p.hybrid) {
+        sink.hbinom = p.binom;
+        sink.hL = p.binom_dim;
+        sink.hT = p.t;
+        sink.hshift = p.hshift;
+        sink.hvis = s_hvis + warp;
+        sink.hover = p.hybrid_over;
+    }
     if ((tid & 31) == 0) {
         sink.hc[0] = 0;
         sink.hc[1] = 0;
+        s_hvis[warp] = 0;
         if (sink.gq) atomicAdd(p.gq.ctl + 3, 1);  // busy: this warp may push to the warp tier
     }
 
@@ -484,13 +529,16 @@ __global__ void __launch_bounds__(BLOCK) k_count(CountParams p) {
         if (MODE == MODE_ORIENT) {
             orient_task<BLOCK, WPL>(p, rows, d, F, list, cbuf, SS, &s_next, acc, visits, work);
         } else {
+            const ull v0 = visits;
             pivot_task<BLOCK, WPL>(p, rows, d, S0, P0, F, list, SS, sink, q, &s_next, &s_piv0,
                                    s_key, visits, work);
+            if (p.hybrid) visits = v0;  // pivot nodes are not orientation visits (sink.hvis)
         }
         work = wt0 + (work - wt0) * ull((d + 31) >> 5);
     }
     __syncthreads();
     if (MODE == MODE_PIVOT) sink.flush(tid & 31);
+    if (MODE == MODE_PIVOT && p.hybrid && (tid & 31) == 0) visits += s_hvis[warp];
     if (sink.gq && (tid & 31) == 0) {
         atomicSub(p.gq.ctl + 3, 1);  // no longer busy (pushed items are drained by thieves)
     }
@@ -986,6 +1034,25 @@ __global__ void k_make_triples(const int64_t *__restrict__ orow, const int32_t *
     }
 }
 
+// C(n, r) for n, r < L, saturating at 2^64 - 1 (the orientation-visit weights
+// of the hybrid CTA tier); rows computed up to n/2 and mirrored
+__global__ void k_binom_table(int L, ull *__restrict__ tab) {
+    for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < L; n += gridDim.x * blockDim.x) {
+        unsigned __int128 c = 1;
+        bool sat = false;
+        for (int r = 0; r <= n / 2; ++r) {
+            const ull v = sat ? ~0ull : ull(c);
+            tab[int64_t(n) * L + r] = v;
+            tab[int64_t(n) * L + (n - r)] = v;
+            if (!sat) {
+                c = c * unsigned(n - r) / unsigned(r + 1);
+                sat = (c >> 64) != 0;
+            }
+        }
+        for (int r = n + 1; r < L; ++r) tab[int64_t(n) * L + r] = 0;
+    }
+}
+
 // branch tasks of the split pivot tasks: (task, v) for every v of P0, in
 // task order (the biggest tasks' branches first)
 __global__ void k_branch_list(const int32_t *__restrict__ cnt, const int32_t *__restrict__ off,
@@ -1064,7 +1131,7 @@ int64_t build_tasks(kc_graph *g, int scheme, int64_t lo, int64_t hi, int min_d, 
     const int64_t N = scheme == KC_SCHEME_EDGE ? g->m_dir : g->n;
     *n_big = 0;
     if (N == 0) return 0;
-    DevBuf keep(N), key(4 * N), key2(4 * N), ids(4 * N), ids2(4 * N), cnt(8);
+    DevBuf keep(N), key(4 * N), key2(4 * N), ids(4 * N), ids2(4 * N), cnt(16);
     if (scheme == KC_SCHEME_VERTEX) {
         DevBuf flag(4 * N), pos(4 * N);
         k_vertex_flags<<<grid_1d(N, g->num_sms), 256, 0, g->stream>>>(g->orow_ptr, N,
@@ -1163,6 +1230,11 @@ void launch_wpl(kc_graph *g, CountParams &p, int grid_override, Keep &keep,
                    size_t(NW) * (dpad + 32 * WPL + kct::kSmallWords + hist_words +
                                  size_t(nsm) * p.fw);
         if (p.scheme == KC_SCHEME_EDGE) w = std::max(w, dpad);
+        if (MODE != MODE_PIVOT) {
+            size_t hs = 2;  // build_task's hash table: H >= 2 dcap slots, 1.5 words each
+            while (hs < 2 * size_t(p.dcap)) hs <<= 1;
+            w = std::max(w, hs + hs / 2);
+        }
         return w;
     };
     // as many shared frames as fit the target budget (at least 4, at most need)
@@ -1285,13 +1357,19 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
                KC_EINVAL, "group_size must be 0 (auto) or a power of two <= 32");
     const bool pivot = a->algorithm == KC_ALGO_PIVOT;
     const int t = a->scheme == KC_SCHEME_VERTEX ? a->k - 1 : a->k - 2;
-    const int64_t L = g->d_max + 2;
+    // orientation: the CTA tier (tasks above 128 locals) counts by pivoting
+    // when the caller passes a histogram of (d_max + 4)^2 cells (hybrid)
+    static const int hybrid_min_t = [] {
+        const char *e = getenv("KC_HYBRID_MIN_T");
+        return e && *e ? atoi(e) : 3;  // 0: off
+    }();
+    const bool hybrid = !pivot && hist && hybrid_min_t > 0 &&
+                        hist_cap >= (g->d_max + 4) * (g->d_max + 4);
+    const int64_t L = pivot ? g->d_max + 2 : (hybrid ? g->d_max + 4 : 0);
     memset(raw, 0, sizeof(*raw));
-    raw->hist_dim = pivot ? L : 0;
-    if (pivot) {
-        KC_REQUIRE(hist && hist_cap >= L * L, KC_EINVAL, "histogram buffer too small");
-        memset(hist, 0, sizeof(uint64_t) * size_t(L * L));
-    }
+    raw->hist_dim = L;
+    if (pivot) KC_REQUIRE(hist && hist_cap >= L * L, KC_EINVAL, "histogram buffer too small");
+    if (L) memset(hist, 0, sizeof(uint64_t) * size_t(L * L));
     if (visits_per_sm) memset(visits_per_sm, 0, sizeof(uint64_t) * size_t(n_sm));
     kc_device_guard guard(g->device);
     StreamScope scope(g->stream);
@@ -1342,8 +1420,14 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
 
     DevBuf outs(8 * size_t(kOutWords));
     KC_CUDA(cudaMemsetAsync(outs.p, 0, 8 * size_t(kOutWords), g->stream));
-    DevBuf dhist(pivot ? 8 * size_t(L * L) : 8);
-    if (pivot) KC_CUDA(cudaMemsetAsync(dhist.p, 0, 8 * size_t(L * L), g->stream));
+    DevBuf dhist(L ? 8 * size_t(L * L) : 8);
+    if (L) KC_CUDA(cudaMemsetAsync(dhist.p, 0, 8 * size_t(L * L), g->stream));
+    DevBuf binom(hybrid ? 8 * size_t(g->d_max + 2) * size_t(g->d_max + 2) : 8);
+    if (hybrid) {
+        const int bl = int(g->d_max + 2);
+        k_binom_table<<<(bl + 127) / 128, 128, 0, g->stream>>>(bl, binom.as<ull>());
+        KC_CUDA(cudaGetLastError());
+    }
 
     CountParams p;
     memset(&p, 0, sizeof(p));
@@ -1362,6 +1446,9 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
     p.hist = dhist.as<ull>();
     p.sh_hl = int(std::min<int64_t>(L, 48));
     ull *o = outs.as<ull>();
+    p.binom = binom.as<ull>();
+    p.binom_dim = int(g->d_max + 2);
+    p.hybrid_over = reinterpret_cast<int *>(o + kOutGq) + 7;  // last queue control word
     p.task_counter = o;
     p.limbs = o + 1;
     p.visits_total = o + 5;
@@ -1382,6 +1469,19 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
     // brings them back with the counters: the host checks the queue drained
     p.gq.ctl = reinterpret_cast<int *>(o + kOutGq);
     p.gq.cap = kGqCap;
+    // CTA tier of the orientation engine: tasks with target T >= hybrid_min_t
+    // are counted by pivoting (the sink turns leaves into the orientation
+    // engine's counts and visits exactly), the rest by the orientation walk
+    auto cta_orient = [&](CountParams b, Keep &kp) {
+        if (hybrid && b.t >= hybrid_min_t) {
+            b.hybrid = 1;
+            b.hshift = t - b.t;
+            b.use_gq = 0;
+            launch<MODE_PIVOT>(g, b, 0, kp, g->stream);
+        } else {
+            launch<MODE_ORIENT>(g, b, 0, kp, g->stream);
+        }
+    };
     // GPU-wide subtree hand-over for the pivot engine (KC_GQ=0 turns it off)
     static const bool gq_on = [] {
         const char *e = getenv("KC_GQ");
@@ -1429,7 +1529,7 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
             b.tasks = items.as<int32_t>();
             b.n_tasks = n_items_big;
             b.task_counter = o + 8 + kSmidSlots + 6;
-            launch<MODE_ORIENT>(g, b, 0, keep, g->stream);
+            cta_orient(b, keep);
         }
         if (n_items_big > 0 && t >= 6) {
             DevBuf sizes(4 * size_t(n_items_big)), offs(4 * size_t(n_items_big));
@@ -1491,7 +1591,7 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
             CountParams b = p;
             b.n_tasks = n_big;
             if (pivot) launch<MODE_PIVOT>(g, b, 0, keep, g->stream);
-            else launch<MODE_ORIENT>(g, b, 0, keep, g->stream);
+            else cta_orient(b, keep);
         }
         int64_t first = n_big;  // warp-tier tasks not yet launched
         if (pivot && n_split > 0) {
@@ -1574,7 +1674,7 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
             b.n_tasks = int64_t(n_ovf);
             b.task_counter = o + 8 + kSmidSlots + 4;
             if (pivot) launch<MODE_PIVOT>(g, b, 0, keep, g->stream);
-            else launch<MODE_ORIENT>(g, b, 0, keep, g->stream);
+            else cta_orient(b, keep);
         }
     }
     KC_CUDA(cudaEventRecord(e_join, g->aux));
@@ -1590,7 +1690,7 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
 
     std::vector<ull> h(kOutWords);
     KC_CUDA(cudaMemcpyAsync(h.data(), outs.p, 8 * h.size(), cudaMemcpyDeviceToHost, g->stream));
-    if (pivot)
+    if (L)
         KC_CUDA(cudaMemcpyAsync(hist, dhist.p, 8 * size_t(L * L), cudaMemcpyDeviceToHost,
                                 g->stream));
     KC_CUDA(cudaStreamSynchronize(g->stream));
@@ -1598,6 +1698,8 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
     memcpy(gq_ctl, &h[kOutGq], sizeof(gq_ctl));
     // every handed-over subtree must have been walked (its leaves are in hist)
     KC_REQUIRE(gq_ctl[1] == 0, KC_ECUDA, "subtree queue not drained at kernel exit");
+    KC_REQUIRE(gq_ctl[7] == 0, KC_EOVERFLOW,
+               "orientation visit counter exceeded 64 bits in a pivot-counted task");
     raw->word_ops = h[8 + kSmidSlots];
     raw->extract_bytes = h[9 + kSmidSlots];
     for (int i = 0; i < 4; ++i) raw->limbs[i] = h[1 + i];

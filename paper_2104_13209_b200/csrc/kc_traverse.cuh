@@ -822,6 +822,31 @@ struct PivotLeafSink {
     const int32_t *l2g;  // local id -> global vertex id of the current universe
     int *hc;             // per-warp smem: [0] countdown [1] cached hungry
     int push_min = kPushMin, cooldown = kPushCooldown, room_min = kPushRoom;
+    // Orientation by pivoting (hybrid): a leaf (len, np) stands for C(np, len - j)
+    // j-cliques of the task, so the orientation engine's visits of the task
+    // (one per j-clique, j = 1..T-1, engine_orient.py:56-79) are the sum of
+    // those; the leaf is binned at len + hshift so the host expands every
+    // task's t-cliques with one t.  hbinom: C(n, r) saturating, hL x hL.
+    const ull *hbinom = nullptr;
+    int hL = 0, hT = 0, hshift = 0;
+    ull *hvis = nullptr;  // per-warp orientation visits (lane 0 adds)
+    int *hover = nullptr; // saturation flag
+    __device__ __forceinline__ int hybrid_leaf(int len, int np) const {
+        ull v = 0;
+        bool ov = false;
+        for (int j = 1; j < hT; ++j) {
+            const int r = len - j;
+            if (r < 0 || r > np) continue;
+            const ull c = hbinom[int64_t(np) * hL + r];
+            const ull nv = v + c;
+            ov |= c == ~0ull || nv < v;
+            v = nv;
+        }
+        const ull o = *hvis;
+        *hvis = o + v;
+        if (ov || o + v < o) *hover = 1;
+        return len + hshift;
+    }
     // uniform: should a child of n members be handed to a hungry warp?
     // Rate-limited: at most one hand-over per kPushCooldown decisions, so a
     // donor keeps doing its own work and thieves get substantial subtrees.
@@ -898,6 +923,7 @@ struct PivotLeafSink {
         return true;
     }
     __device__ __forceinline__ void add(int len, int np) const {
+        if (hbinom) len = hybrid_leaf(len, np);
         if (len < kLeafHL) {
             uint32_t &c = whist[len * (len + 1) / 2 + np];
             if (++c == 0x80000000u) {

@@ -16,3 +16,5 @@ timeout 900 python scripts/explore.py --workload rmat16 --k 10 --algo pivot --sc
 timeout 300 python scripts/exact_order_check.py rmat18 rmat22 >> $J 2>&1
 timeout 600 python scripts/explore.py --workload rmat18 --k 4 7 --algo orient --scheme vertex --criterion degeneracy --reps 2 >> $J 2>&1
 echo done >> $J
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r2_launches_rmat20_k7.csv \
+  python scripts/explore.py --workload rmat20 --k 7 --algo orient --scheme vertex --criterion degeneracy --reps 1 > gpurun_out/r2_launches_rmat20_k7.log 2>&1
