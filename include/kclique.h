@@ -152,8 +152,7 @@ typedef struct {
     uint64_t limbs[4];      /* 32-bit limb sums of the direct (orient / t<=1) count */
     uint64_t visits;        /* tree nodes expanded (reference load.total) */
     uint64_t tasks_run;     /* tasks with enough locals */
-    int64_t hist_dim;       /* L: hist is L x L u64 (pivot; orientation when its CTA
-                               tier counted by pivoting), else 0 */
+    int64_t hist_dim;       /* L: hist is L x L u64 (pivot), 0 for orient */
     double count_ms;        /* device time of the counting kernels */
     int32_t group_size;     /* lanes per sub-warp group the orientation warp tier ran with */
     int32_t launches;       /* counting-kernel launches of this call */
@@ -161,10 +160,7 @@ typedef struct {
     uint64_t extract_bytes; /* roofline: global bytes read by the sub-graph builder */
 } kc_count_raw;
 
-/* hist: caller buffer of hist_cap u64: pivot L*L with L = d_max + 2 (required);
- * orientation (optional) L = d_max + 4 -- given, tasks above 128 locals are
- * counted by pivoting (exact counts and orientation visits, hist_dim = L);
- * NULL, every task walks the orientation tree;
+/* hist: caller buffer of hist_cap u64 (L*L, L = d_max + 2) or NULL for orient;
  * visits_per_sm: caller buffer of n_sm u64 or NULL.  Limits: the bitmap
  * engines hold at most 4096 locals per task (oriented max out-degree <= 4096,
  * else KC_EINVAL); counts are exact to 2^128 (KC_EOVERFLOW beyond). */

@@ -93,11 +93,11 @@ def run_tasks_gpu(g, cfg, ranking, device=0):
         pivot = cfg.algorithm == "pivot"
         a = _Args(cfg.k, 1 if pivot else 0, 1 if cfg.scheme == "edge" else 0, 0, 0, 0, 0, -1)
         raw = _Raw()
-        # leaf histogram: pivot, and the orientation tasks kc_count counts by
-        # pivoting (its CTA tier); hist_dim tells which cells were used
-        dim = int(info.d_max) + (2 if pivot else 4)
-        hist = np.zeros(dim * dim, dtype=np.uint64)
-        _check(L.kc_count(h, ctypes.byref(a), ctypes.byref(raw), _ptr(hist), hist.size, None, 0))
+        # pivot: (length, pivots) leaf histogram, expanded exactly below
+        dim = int(info.d_max) + 2
+        hist = np.zeros(dim * dim if pivot else 1, dtype=np.uint64)
+        _check(L.kc_count(h, ctypes.byref(a), ctypes.byref(raw), _ptr(hist) if pivot else None,
+                          hist.size if pivot else 0, None, 0))
     finally:
         L.kc_graph_free(h)
     # exact count: 32-bit limb sums, plus (pivot) sum of hist[len, np] * C(np, len - t)

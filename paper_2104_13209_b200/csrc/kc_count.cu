@@ -51,12 +51,6 @@ struct CountParams {
                             // pivot branch tasks: the root branch v (local index)
     int branch;             // pivot: tasks are root branches (task, v) of split tasks
     int roots_only;         // pivot: compute the root frame of each task (split pass)
-    // orientation tasks counted by the pivot engine (CTA tier): t = the task
-    // target T, leaves binned at len + hshift, orientation visits from binom
-    int hybrid, hshift;
-    const ull *binom;
-    int binom_dim;
-    int *hybrid_over;
     const int32_t *branch_si;   // branch task -> split-task index
     int32_t *root_piv;          // split task -> root pivot (local index)
     uint32_t *root_P;           // split task -> root branch set P0 (4 words)
@@ -434,16 +428,18 @@ __global__ void __launch_bounds__(BLOCK) k_count(CountParams p) {
     q.items = area + 64 * WPL;
     if (MODE == MODE_PIVOT) area += 64 * WPL + kStealCap * (32 * WPL + 4);
     const int hist_cells = MODE == MODE_PIVOT ? kct::kLeafCells : 0;
+    const int mid_words = MODE == MODE_ORIENT ? kct::kMidWords : 0;
     const int per_warp = ((p.dcap + 3) & ~3) + 32 * WPL + kct::kSmallWords + hist_cells +
-                         p.nsm_frames * p.fw;
+                         mid_words + p.nsm_frames * p.fw;
     int *list = reinterpret_cast<int *>(area + warp * per_warp);
     uint32_t *cbuf = area + warp * per_warp + ((p.dcap + 3) & ~3);
     kct::SmallScratch SS;
     SS.srow = cbuf + 32 * WPL;
     SS.sstk = SS.srow + 32;
     uint32_t *whist = SS.srow + kct::kSmallWords;
+    if (MODE == MODE_ORIENT) SS.mrow = whist + hist_cells;  // <= 128-member pair levels
     kct::Frames F;
-    F.sm = whist + hist_cells;
+    F.sm = whist + hist_cells + mid_words;
     F.nsm = p.nsm_frames;
     F.fw = p.fw;
     F.gm = p.frames_global ? p.frames_global + (int64_t(blockIdx.x) * NW + warp) * p.frames_slot
@@ -460,19 +456,9 @@ __global__ void __launch_bounds__(BLOCK) k_count(CountParams p) {
     sink.push_min = p.gq_push_min;
     sink.cooldown = p.gq_cooldown;
     sink.room_min = p.gq_room;
-    __shared__ ull s_hvis[NW];
-    if (MODE == MODE_PIVOT && p.hybrid) {
-        sink.hbinom = p.binom;
-        sink.hL = p.binom_dim;
-        sink.hT = p.t;
-        sink.hshift = p.hshift;
-        sink.hvis = s_hvis + warp;
-        sink.hover = p.hybrid_over;
-    }
     if ((tid & 31) == 0) {
         sink.hc[0] = 0;
         sink.hc[1] = 0;
-        s_hvis[warp] = 0;
         if (sink.gq) atomicAdd(p.gq.ctl + 3, 1);  // busy: this warp may push to the warp tier
     }
 
@@ -529,16 +515,13 @@ __global__ void __launch_bounds__(BLOCK) k_count(CountParams p) {
         if (MODE == MODE_ORIENT) {
             orient_task<BLOCK, WPL>(p, rows, d, F, list, cbuf, SS, &s_next, acc, visits, work);
         } else {
-            const ull v0 = visits;
             pivot_task<BLOCK, WPL>(p, rows, d, S0, P0, F, list, SS, sink, q, &s_next, &s_piv0,
                                    s_key, visits, work);
-            if (p.hybrid) visits = v0;  // pivot nodes are not orientation visits (sink.hvis)
         }
         work = wt0 + (work - wt0) * ull((d + 31) >> 5);
     }
     __syncthreads();
     if (MODE == MODE_PIVOT) sink.flush(tid & 31);
-    if (MODE == MODE_PIVOT && p.hybrid && (tid & 31) == 0) visits += s_hvis[warp];
     if (sink.gq && (tid & 31) == 0) {
         atomicSub(p.gq.ctl + 3, 1);  // no longer busy (pushed items are drained by thieves)
     }
@@ -1034,25 +1017,6 @@ __global__ void k_make_triples(const int64_t *__restrict__ orow, const int32_t *
     }
 }
 
-// C(n, r) for n, r < L, saturating at 2^64 - 1 (the orientation-visit weights
-// of the hybrid CTA tier); rows computed up to n/2 and mirrored
-__global__ void k_binom_table(int L, ull *__restrict__ tab) {
-    for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < L; n += gridDim.x * blockDim.x) {
-        unsigned __int128 c = 1;
-        bool sat = false;
-        for (int r = 0; r <= n / 2; ++r) {
-            const ull v = sat ? ~0ull : ull(c);
-            tab[int64_t(n) * L + r] = v;
-            tab[int64_t(n) * L + (n - r)] = v;
-            if (!sat) {
-                c = c * unsigned(n - r) / unsigned(r + 1);
-                sat = (c >> 64) != 0;
-            }
-        }
-        for (int r = n + 1; r < L; ++r) tab[int64_t(n) * L + r] = 0;
-    }
-}
-
 // branch tasks of the split pivot tasks: (task, v) for every v of P0, in
 // task order (the biggest tasks' branches first)
 __global__ void k_branch_list(const int32_t *__restrict__ cnt, const int32_t *__restrict__ off,
@@ -1228,6 +1192,7 @@ void launch_wpl(kc_graph *g, CountParams &p, int grid_override, Keep &keep,
     auto area_words = [&](int nsm) {
         size_t w = (MODE == MODE_PIVOT ? 64 * WPL + kStealCap * (32 * WPL + 4) : 0) +
                    size_t(NW) * (dpad + 32 * WPL + kct::kSmallWords + hist_words +
+                                 (MODE == MODE_ORIENT ? kct::kMidWords : 0) +
                                  size_t(nsm) * p.fw);
         if (p.scheme == KC_SCHEME_EDGE) w = std::max(w, dpad);
         if (MODE != MODE_PIVOT) {
@@ -1357,19 +1322,13 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
                KC_EINVAL, "group_size must be 0 (auto) or a power of two <= 32");
     const bool pivot = a->algorithm == KC_ALGO_PIVOT;
     const int t = a->scheme == KC_SCHEME_VERTEX ? a->k - 1 : a->k - 2;
-    // orientation: the CTA tier (tasks above 128 locals) counts by pivoting
-    // when the caller passes a histogram of (d_max + 4)^2 cells (hybrid)
-    static const int hybrid_min_t = [] {
-        const char *e = getenv("KC_HYBRID_MIN_T");
-        return e && *e ? atoi(e) : 3;  // 0: off
-    }();
-    const bool hybrid = !pivot && hist && hybrid_min_t > 0 &&
-                        hist_cap >= (g->d_max + 4) * (g->d_max + 4);
-    const int64_t L = pivot ? g->d_max + 2 : (hybrid ? g->d_max + 4 : 0);
+    const int64_t L = pivot ? g->d_max + 2 : 0;
     memset(raw, 0, sizeof(*raw));
     raw->hist_dim = L;
-    if (pivot) KC_REQUIRE(hist && hist_cap >= L * L, KC_EINVAL, "histogram buffer too small");
-    if (L) memset(hist, 0, sizeof(uint64_t) * size_t(L * L));
+    if (pivot) {
+        KC_REQUIRE(hist && hist_cap >= L * L, KC_EINVAL, "histogram buffer too small");
+        memset(hist, 0, sizeof(uint64_t) * size_t(L * L));
+    }
     if (visits_per_sm) memset(visits_per_sm, 0, sizeof(uint64_t) * size_t(n_sm));
     kc_device_guard guard(g->device);
     StreamScope scope(g->stream);
@@ -1422,12 +1381,6 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
     KC_CUDA(cudaMemsetAsync(outs.p, 0, 8 * size_t(kOutWords), g->stream));
     DevBuf dhist(L ? 8 * size_t(L * L) : 8);
     if (L) KC_CUDA(cudaMemsetAsync(dhist.p, 0, 8 * size_t(L * L), g->stream));
-    DevBuf binom(hybrid ? 8 * size_t(g->d_max + 2) * size_t(g->d_max + 2) : 8);
-    if (hybrid) {
-        const int bl = int(g->d_max + 2);
-        k_binom_table<<<(bl + 127) / 128, 128, 0, g->stream>>>(bl, binom.as<ull>());
-        KC_CUDA(cudaGetLastError());
-    }
 
     CountParams p;
     memset(&p, 0, sizeof(p));
@@ -1446,9 +1399,6 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
     p.hist = dhist.as<ull>();
     p.sh_hl = int(std::min<int64_t>(L, 48));
     ull *o = outs.as<ull>();
-    p.binom = binom.as<ull>();
-    p.binom_dim = int(g->d_max + 2);
-    p.hybrid_over = reinterpret_cast<int *>(o + kOutGq) + 7;  // last queue control word
     p.task_counter = o;
     p.limbs = o + 1;
     p.visits_total = o + 5;
@@ -1469,19 +1419,6 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
     // brings them back with the counters: the host checks the queue drained
     p.gq.ctl = reinterpret_cast<int *>(o + kOutGq);
     p.gq.cap = kGqCap;
-    // CTA tier of the orientation engine: tasks with target T >= hybrid_min_t
-    // are counted by pivoting (the sink turns leaves into the orientation
-    // engine's counts and visits exactly), the rest by the orientation walk
-    auto cta_orient = [&](CountParams b, Keep &kp) {
-        if (hybrid && b.t >= hybrid_min_t) {
-            b.hybrid = 1;
-            b.hshift = t - b.t;
-            b.use_gq = 0;
-            launch<MODE_PIVOT>(g, b, 0, kp, g->stream);
-        } else {
-            launch<MODE_ORIENT>(g, b, 0, kp, g->stream);
-        }
-    };
     // GPU-wide subtree hand-over for the pivot engine (KC_GQ=0 turns it off)
     static const bool gq_on = [] {
         const char *e = getenv("KC_GQ");
@@ -1529,7 +1466,7 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
             b.tasks = items.as<int32_t>();
             b.n_tasks = n_items_big;
             b.task_counter = o + 8 + kSmidSlots + 6;
-            cta_orient(b, keep);
+            launch<MODE_ORIENT>(g, b, 0, keep, g->stream);
         }
         if (n_items_big > 0 && t >= 6) {
             DevBuf sizes(4 * size_t(n_items_big)), offs(4 * size_t(n_items_big));
@@ -1591,7 +1528,7 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
             CountParams b = p;
             b.n_tasks = n_big;
             if (pivot) launch<MODE_PIVOT>(g, b, 0, keep, g->stream);
-            else cta_orient(b, keep);
+            else launch<MODE_ORIENT>(g, b, 0, keep, g->stream);
         }
         int64_t first = n_big;  // warp-tier tasks not yet launched
         if (pivot && n_split > 0) {
@@ -1674,7 +1611,7 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
             b.n_tasks = int64_t(n_ovf);
             b.task_counter = o + 8 + kSmidSlots + 4;
             if (pivot) launch<MODE_PIVOT>(g, b, 0, keep, g->stream);
-            else cta_orient(b, keep);
+            else launch<MODE_ORIENT>(g, b, 0, keep, g->stream);
         }
     }
     KC_CUDA(cudaEventRecord(e_join, g->aux));
@@ -1698,8 +1635,6 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
     memcpy(gq_ctl, &h[kOutGq], sizeof(gq_ctl));
     // every handed-over subtree must have been walked (its leaves are in hist)
     KC_REQUIRE(gq_ctl[1] == 0, KC_ECUDA, "subtree queue not drained at kernel exit");
-    KC_REQUIRE(gq_ctl[7] == 0, KC_EOVERFLOW,
-               "orientation visit counter exceeded 64 bits in a pivot-counted task");
     raw->word_ops = h[8 + kSmidSlots];
     raw->extract_bytes = h[9 + kSmidSlots];
     for (int i = 0; i < 4; ++i) raw->limbs[i] = h[1 + i];

@@ -322,6 +322,67 @@ __device__ __forceinline__ void score_pairs4(const uint32_t *__restrict__ rows, 
     __syncwarp();
 }
 
+// Pair level of a wide task (rows of W > 4 words, the CTA tier) whose set X
+// has 33..128 members: relabel X's members 0..n-1 (ascending local id) and
+// compress their rows restricted to X into 16-byte rows (mrow), then run the
+// warp tier's four-word pair loop over them.  Member j of row i is found by
+// walking the set bits of X & row i word by word, its new index being the
+// count of X's members below it (per-word prefix counts) -- the work is one
+// step per (i, j) edge inside X, the pair count the loop would walk anyway.
+// Counts and visits are order-free sums, hence unchanged.
+template <int WPL>
+__device__ __forceinline__ void score_pairs_mid(const uint32_t *__restrict__ rows, int RS, int W,
+                                                const Set<WPL> &X, int *list, uint32_t *cbuf,
+                                                uint32_t *mrow, int lane, ull &acc, ull &visits,
+                                                ull &work) {
+    const int n = compact<WPL>(X, list, lane, W);
+    uint32_t *cum = mrow + 128 * 4;  // exclusive prefix popcount of X's words
+    int carry = 0;
+#pragma unroll
+    for (int p = 0; p < WPL; ++p) {
+        const int c = __popc(X.w[p]);
+        int incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl += y;
+        }
+        cbuf[p * 32 + lane] = X.w[p];
+        cum[p * 32 + lane] = uint32_t(carry + incl - c);
+        carry += __shfl_sync(FULL, incl, 31);
+    }
+    __syncwarp();
+    for (int i = lane; i < n; i += 32) {
+        const uint32_t *ri = rows + list[i] * RS;
+        uint32_t c0 = 0, c1 = 0, c2 = 0, c3 = 0;
+        for (int w = 0; w < W; ++w) {
+            const uint32_t xw = cbuf[w];
+            uint32_t m = xw & ri[w];
+            if (!m) continue;
+            const int base = int(cum[w]);
+            while (m) {
+                const int b = __ffs(m) - 1;
+                m &= m - 1u;
+                const int j = base + __popc(xw & ((1u << b) - 1u));
+                const uint32_t bit = 1u << (j & 31);
+                const int q = j >> 5;
+                c0 |= q == 0 ? bit : 0u;
+                c1 |= q == 1 ? bit : 0u;
+                c2 |= q == 2 ? bit : 0u;
+                c3 |= q == 3 ? bit : 0u;
+            }
+        }
+        *reinterpret_cast<uint4 *>(mrow + (i << 2)) = make_uint4(c0, c1, c2, c3);
+    }
+    __syncwarp();
+    Set<1> all;
+    {
+        const int lo = lane << 5;
+        all.w[0] = lo >= n ? 0u : (lo + 32 <= n ? FULL : ((1u << (n - lo)) - 1u));
+    }
+    score_pairs4(mrow, all, list, lane, acc, visits, work);
+}
+
 template <int WPL>
 __device__ __forceinline__ void score_pairs(const uint32_t *__restrict__ rows, int RS, int W,
                                             const Set<WPL> &C, int *list, uint32_t *cbuf,
@@ -822,31 +883,6 @@ struct PivotLeafSink {
     const int32_t *l2g;  // local id -> global vertex id of the current universe
     int *hc;             // per-warp smem: [0] countdown [1] cached hungry
     int push_min = kPushMin, cooldown = kPushCooldown, room_min = kPushRoom;
-    // Orientation by pivoting (hybrid): a leaf (len, np) stands for C(np, len - j)
-    // j-cliques of the task, so the orientation engine's visits of the task
-    // (one per j-clique, j = 1..T-1, engine_orient.py:56-79) are the sum of
-    // those; the leaf is binned at len + hshift so the host expands every
-    // task's t-cliques with one t.  hbinom: C(n, r) saturating, hL x hL.
-    const ull *hbinom = nullptr;
-    int hL = 0, hT = 0, hshift = 0;
-    ull *hvis = nullptr;  // per-warp orientation visits (lane 0 adds)
-    int *hover = nullptr; // saturation flag
-    __device__ __forceinline__ int hybrid_leaf(int len, int np) const {
-        ull v = 0;
-        bool ov = false;
-        for (int j = 1; j < hT; ++j) {
-            const int r = len - j;
-            if (r < 0 || r > np) continue;
-            const ull c = hbinom[int64_t(np) * hL + r];
-            const ull nv = v + c;
-            ov |= c == ~0ull || nv < v;
-            v = nv;
-        }
-        const ull o = *hvis;
-        *hvis = o + v;
-        if (ov || o + v < o) *hover = 1;
-        return len + hshift;
-    }
     // uniform: should a child of n members be handed to a hungry warp?
     // Rate-limited: at most one hand-over per kPushCooldown decisions, so a
     // donor keeps doing its own work and thieves get substantial subtrees.
@@ -923,7 +959,6 @@ struct PivotLeafSink {
         return true;
     }
     __device__ __forceinline__ void add(int len, int np) const {
-        if (hbinom) len = hybrid_leaf(len, np);
         if (len < kLeafHL) {
             uint32_t &c = whist[len * (len + 1) / 2 + np];
             if (++c == 0x80000000u) {
@@ -1208,7 +1243,9 @@ struct SmallScratch {
     uint32_t *sstk;  // kMapWords words: LocalMap storage
     uint2 *nstk = nullptr;  // pivot per-lane node stack (warp tier), nullptr: uniform walks
     int ncap = 0;
+    uint32_t *mrow = nullptr;  // kMidWords: compressed <= 128-member pair level (CTA tier)
 };
+constexpr int kMidWords = 128 * 4 + 128;  // 128 rows of 4 words + per-word prefix counts
 constexpr int kNodeCap = 512;  // pivot_lanes stack capacity (nodes of 2 words)
 constexpr int kMapSlots = 256;
 constexpr int kMapWords = kMapSlots + kMapSlots / 4;
@@ -1286,7 +1323,10 @@ __device__ void orient_subtree(const uint32_t *__restrict__ rows, int RS, int W,
     if (orient_try_small<WPL, G>(rows, RS, W, C, 1, last, list, SS, lane, acc, visits, work))
         return;
     if (last == 2) {  // frame 1 is the next-to-last level
-        score_pairs<WPL>(rows, RS, W, C, list, cbuf, lane, acc, visits, work);
+        if (W > 4 && SS.mrow && warp_count<WPL>(C) <= 128)
+            score_pairs_mid<WPL>(rows, RS, W, C, list, cbuf, SS.mrow, lane, acc, visits, work);
+        else
+            score_pairs<WPL>(rows, RS, W, C, list, cbuf, lane, acc, visits, work);
         return;
     }
     int s = 1;
@@ -1320,7 +1360,11 @@ __device__ void orient_subtree(const uint32_t *__restrict__ rows, int RS, int W,
                                      work))
             continue;
         if (s + 2 == last) {  // X is the next-to-last frame
-            score_pairs<WPL>(rows, RS, W, X, list, cbuf, lane, acc, visits, work);
+            if (W > 4 && SS.mrow && warp_count<WPL>(X) <= 128)
+                score_pairs_mid<WPL>(rows, RS, W, X, list, cbuf, SS.mrow, lane, acc, visits,
+                                     work);
+            else
+                score_pairs<WPL>(rows, RS, W, X, list, cbuf, lane, acc, visits, work);
             continue;
         }
         uint32_t *f = F.at(s);

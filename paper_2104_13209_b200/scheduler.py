@@ -157,15 +157,15 @@ def device_count_raw(og, cfg: RunConfig, task_lo: int = 0, task_hi: int = -1) ->
                          int(task_hi))
     raw = _lib.KcCountRaw()
     pivot = cfg.algorithm == "pivot"
-    # pivot: the (length, pivots) leaf histogram; orientation: the same for
-    # the tasks its CTA tier counts by pivoting (kc_count's hybrid tier)
-    dim = og.d_max + (2 if pivot else 4)
-    hist = np.zeros(dim * dim, dtype=np.uint64)
+    # pivot: the (length, pivots) leaf histogram, expanded on the host
+    dim = og.d_max + 2
+    hist = np.zeros(dim * dim if pivot else 1, dtype=np.uint64)
     # fixed width (every rank's vector has the same length for the all-reduce);
     # trimmed to the SMs actually used only when reported (used_sms)
     per_sm = np.zeros(SM_SLOTS, dtype=np.uint64)
-    _lib.check(L.kc_count(h, ctypes.byref(a), ctypes.byref(raw), _lib._ptr(hist),
-                          hist.size, _lib._ptr(per_sm), per_sm.size))
+    _lib.check(L.kc_count(h, ctypes.byref(a), ctypes.byref(raw),
+                          _lib._ptr(hist) if pivot else None, hist.size if pivot else 0,
+                          _lib._ptr(per_sm), per_sm.size))
     hd = int(raw.hist_dim)
     return RawCount(np.array(raw.limbs[:], dtype=np.uint64), int(raw.visits), int(raw.tasks_run),
                     hist[:hd * hd].reshape(hd, hd) if hd else None, per_sm,
