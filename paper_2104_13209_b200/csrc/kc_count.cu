@@ -428,7 +428,8 @@ __global__ void __launch_bounds__(BLOCK) k_count(CountParams p) {
     q.items = area + 64 * WPL;
     if (MODE == MODE_PIVOT) area += 64 * WPL + kStealCap * (32 * WPL + 4);
     const int hist_cells = MODE == MODE_PIVOT ? kct::kLeafCells : 0;
-    const int mid_words = MODE == MODE_ORIENT ? kct::kMidWords : 0;
+    // compressed pair-level rows: only where a pair level exists (t >= 4)
+    const int mid_words = (MODE == MODE_ORIENT && p.t >= 4) ? kct::kMidWords : 0;
     const int per_warp = ((p.dcap + 3) & ~3) + 32 * WPL + kct::kSmallWords + hist_cells +
                          mid_words + p.nsm_frames * p.fw;
     int *list = reinterpret_cast<int *>(area + warp * per_warp);
@@ -437,7 +438,7 @@ __global__ void __launch_bounds__(BLOCK) k_count(CountParams p) {
     SS.srow = cbuf + 32 * WPL;
     SS.sstk = SS.srow + 32;
     uint32_t *whist = SS.srow + kct::kSmallWords;
-    if (MODE == MODE_ORIENT) SS.mrow = whist + hist_cells;  // <= 128-member pair levels
+    if (mid_words) SS.mrow = whist + hist_cells;  // <= 256-member pair levels
     kct::Frames F;
     F.sm = whist + hist_cells + mid_words;
     F.nsm = p.nsm_frames;
@@ -1192,7 +1193,7 @@ void launch_wpl(kc_graph *g, CountParams &p, int grid_override, Keep &keep,
     auto area_words = [&](int nsm) {
         size_t w = (MODE == MODE_PIVOT ? 64 * WPL + kStealCap * (32 * WPL + 4) : 0) +
                    size_t(NW) * (dpad + 32 * WPL + kct::kSmallWords + hist_words +
-                                 (MODE == MODE_ORIENT ? kct::kMidWords : 0) +
+                                 (MODE == MODE_ORIENT && p.t >= 4 ? kct::kMidWords : 0) +
                                  size_t(nsm) * p.fw);
         if (p.scheme == KC_SCHEME_EDGE) w = std::max(w, dpad);
         if (MODE != MODE_PIVOT) {

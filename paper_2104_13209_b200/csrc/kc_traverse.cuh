@@ -171,6 +171,31 @@ __device__ __forceinline__ int compact4(uint32_t c0, uint32_t c1, uint32_t c2, u
     return n;
 }
 
+// members of an eight-word set (words replicated in every lane: c[0..8)):
+// lane L owns bits [8L, 8L+8)
+__device__ __forceinline__ int compact8(const uint32_t (&c)[8], int *list, int lane) {
+    const int wsel = lane >> 2;
+    uint32_t word = c[0];
+#pragma unroll
+    for (int i = 1; i < 8; ++i) word = wsel == i ? c[i] : word;
+    uint32_t byte = (word >> ((lane & 3) << 3)) & 255u;
+    const int cnt = __popc(byte);
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += y;
+    }
+    int off = incl - cnt;
+    while (byte) {
+        list[off++] = (lane << 3) + __ffs(byte) - 1;
+        byte &= byte - 1u;
+    }
+    const int n = __shfl_sync(FULL, incl, 31);
+    __syncwarp();
+    return n;
+}
+
 // compact the members of C (ascending) into list[0..n); returns n (uniform)
 template <int WPL>
 __device__ __forceinline__ int compact(const Set<WPL> &C, int *list, int lane, int W = 32 * WPL) {
@@ -322,10 +347,60 @@ __device__ __forceinline__ void score_pairs4(const uint32_t *__restrict__ rows, 
     __syncwarp();
 }
 
+// score_pairs4 for eight-word rows (stride 8, two LDS.128 per row): the
+// pair level of a CTA-tier set compressed to 129..256 members
+__device__ __forceinline__ void score_pairs8(const uint32_t *__restrict__ rows, int n, int *list,
+                                             int lane, ull &acc, ull &visits, ull &work) {
+    uint32_t c[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int lo = i << 5;
+        c[i] = lo >= n ? 0u : (lo + 32 <= n ? FULL : ((1u << (n - lo)) - 1u));
+    }
+    if (lane == 0) visits += ull(n);
+    unsigned a32 = 0;
+    for (int base = 0; base < n; base += 32) {
+        const int cnt = n - base < 32 ? n - base : 32;
+        const int lg = lanes_per_member_log2(cnt);
+        const int mi = lane >> lg, sub = lane & ((1 << lg) - 1);
+        if (mi >= cnt) continue;
+        const int v = base + mi;  // members are 0..n-1
+        const uint4 ra = *reinterpret_cast<const uint4 *>(rows + (v << 3));
+        const uint4 rb = *reinterpret_cast<const uint4 *>(rows + (v << 3) + 4);
+        const uint32_t cm[8] = {c[0] & ra.x, c[1] & ra.y, c[2] & ra.z, c[3] & ra.w,
+                                c[4] & rb.x, c[5] & rb.y, c[6] & rb.z, c[7] & rb.w};
+        if (sub == 0) {
+            unsigned xs = 0;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) xs += unsigned(__popc(cm[i]));
+            visits += ull(xs);
+            work += 1 + ull(xs);
+        }
+        const uint32_t st = id_stripe(lg, sub);
+        CsaAcc h;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+            uint32_t m = cm[w] & st;
+            while (m) {
+                const int b = 31 - __clz(m);
+                m ^= 1u << b;
+                const uint32_t *rx = rows + (((w << 5) + b) << 3);
+                const uint4 xa = *reinterpret_cast<const uint4 *>(rx);
+                const uint4 xb = *reinterpret_cast<const uint4 *>(rx + 4);
+                h.add4(cm[0] & xa.x, cm[1] & xa.y, cm[2] & xa.z, cm[3] & xa.w);
+                h.add4(cm[4] & xb.x, cm[5] & xb.y, cm[6] & xb.z, cm[7] & xb.w);
+            }
+        }
+        a32 += h.total();
+    }
+    acc += a32;
+    __syncwarp();
+}
+
 // Pair level of a wide task (rows of W > 4 words, the CTA tier) whose set X
-// has 33..128 members: relabel X's members 0..n-1 (ascending local id) and
-// compress their rows restricted to X into 16-byte rows (mrow), then run the
-// warp tier's four-word pair loop over them.  Member j of row i is found by
+// has 33..256 members: relabel X's members 0..n-1 (ascending local id) and
+// compress their rows restricted to X into 16- or 32-byte rows (mrow), then
+// run the four- / eight-word pair loop over them.  Member j of row i is found by
 // walking the set bits of X & row i word by word, its new index being the
 // count of X's members below it (per-word prefix counts) -- the work is one
 // step per (i, j) edge inside X, the pair count the loop would walk anyway.
@@ -336,7 +411,7 @@ __device__ __forceinline__ void score_pairs_mid(const uint32_t *__restrict__ row
                                                 uint32_t *mrow, int lane, ull &acc, ull &visits,
                                                 ull &work) {
     const int n = compact<WPL>(X, list, lane, W);
-    uint32_t *cum = mrow + 128 * 4;  // exclusive prefix popcount of X's words
+    uint32_t *cum = mrow + 256 * 8;  // exclusive prefix popcount of X's words
     int carry = 0;
 #pragma unroll
     for (int p = 0; p < WPL; ++p) {
@@ -352,9 +427,10 @@ __device__ __forceinline__ void score_pairs_mid(const uint32_t *__restrict__ row
         carry += __shfl_sync(FULL, incl, 31);
     }
     __syncwarp();
+    const int RSM = n <= 128 ? 4 : 8;  // compressed row stride (words)
     for (int i = lane; i < n; i += 32) {
         const uint32_t *ri = rows + list[i] * RS;
-        uint32_t c0 = 0, c1 = 0, c2 = 0, c3 = 0;
+        uint32_t cr[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
         for (int w = 0; w < W; ++w) {
             const uint32_t xw = cbuf[w];
             uint32_t m = xw & ri[w];
@@ -366,15 +442,19 @@ __device__ __forceinline__ void score_pairs_mid(const uint32_t *__restrict__ row
                 const int j = base + __popc(xw & ((1u << b) - 1u));
                 const uint32_t bit = 1u << (j & 31);
                 const int q = j >> 5;
-                c0 |= q == 0 ? bit : 0u;
-                c1 |= q == 1 ? bit : 0u;
-                c2 |= q == 2 ? bit : 0u;
-                c3 |= q == 3 ? bit : 0u;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) cr[k] |= q == k ? bit : 0u;
             }
         }
-        *reinterpret_cast<uint4 *>(mrow + (i << 2)) = make_uint4(c0, c1, c2, c3);
+        *reinterpret_cast<uint4 *>(mrow + i * RSM) = make_uint4(cr[0], cr[1], cr[2], cr[3]);
+        if (RSM == 8)
+            *reinterpret_cast<uint4 *>(mrow + i * RSM + 4) = make_uint4(cr[4], cr[5], cr[6], cr[7]);
     }
     __syncwarp();
+    if (RSM == 8) {
+        score_pairs8(mrow, n, list, lane, acc, visits, work);
+        return;
+    }
     Set<1> all;
     {
         const int lo = lane << 5;
@@ -1245,7 +1325,7 @@ struct SmallScratch {
     int ncap = 0;
     uint32_t *mrow = nullptr;  // kMidWords: compressed <= 128-member pair level (CTA tier)
 };
-constexpr int kMidWords = 128 * 4 + 128;  // 128 rows of 4 words + per-word prefix counts
+constexpr int kMidWords = 256 * 8 + 128;  // 256 rows of 8 words + per-word prefix counts
 constexpr int kNodeCap = 512;  // pivot_lanes stack capacity (nodes of 2 words)
 constexpr int kMapSlots = 256;
 constexpr int kMapWords = kMapSlots + kMapSlots / 4;
@@ -1323,7 +1403,7 @@ __device__ void orient_subtree(const uint32_t *__restrict__ rows, int RS, int W,
     if (orient_try_small<WPL, G>(rows, RS, W, C, 1, last, list, SS, lane, acc, visits, work))
         return;
     if (last == 2) {  // frame 1 is the next-to-last level
-        if (W > 4 && SS.mrow && warp_count<WPL>(C) <= 128)
+        if (W > 4 && SS.mrow && warp_count<WPL>(C) <= 256)
             score_pairs_mid<WPL>(rows, RS, W, C, list, cbuf, SS.mrow, lane, acc, visits, work);
         else
             score_pairs<WPL>(rows, RS, W, C, list, cbuf, lane, acc, visits, work);
@@ -1360,7 +1440,7 @@ __device__ void orient_subtree(const uint32_t *__restrict__ rows, int RS, int W,
                                      work))
             continue;
         if (s + 2 == last) {  // X is the next-to-last frame
-            if (W > 4 && SS.mrow && warp_count<WPL>(X) <= 128)
+            if (W > 4 && SS.mrow && warp_count<WPL>(X) <= 256)
                 score_pairs_mid<WPL>(rows, RS, W, X, list, cbuf, SS.mrow, lane, acc, visits,
                                      work);
             else
