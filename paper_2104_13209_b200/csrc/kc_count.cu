@@ -87,7 +87,14 @@ struct CountParams {
     ull *ext_bytes;
     ull *visits_per_sm;
     ull *tasks_run;
+    ull *prof;  // KC_TIMING diagnostics (nullptr: off): see kProf* below
 };
+// prof words: CTA tier build / walk cycles (thread 0), warp tier build / walk
+// cycles (lane 0, summed over warps), then a histogram of overflow task sizes
+// in buckets of 32 locals
+constexpr int kProfCtaBuild = 0, kProfCtaWalk = 1, kProfWarpBuild = 2, kProfWarpWalk = 3,
+              kProfOvfHist = 4, kProfGqIdle = 68, kProfGqWalk = 69, kProfGqItems = 70,
+              kProfWords = 72;
 
 __host__ __device__ __forceinline__ int row_stride(int W) { return W | 1; }
 // warp tier, orientation: rows of 2..4 words padded to 16 bytes so the
@@ -394,6 +401,7 @@ __device__ void pivot_task(const CountParams &p, const uint32_t *rows, int d, ui
 // the persistent kernel
 // ---------------------------------------------------------------------------
 enum Mode { MODE_ORIENT = 0, MODE_PIVOT = 1, MODE_EXTRACT = 2 };
+constexpr int kCtaSmallWords = 32;  // CTA tier per-warp S-tier rows (srow)
 constexpr int kStealCap = 16;  // pivot work-sharing stack slots per CTA
 
 template <int BLOCK, int MODE, int WPL, bool GQ = false>
@@ -429,15 +437,16 @@ __global__ void __launch_bounds__(BLOCK) k_count(CountParams p) {
     if (MODE == MODE_PIVOT) area += 64 * WPL + kStealCap * (32 * WPL + 4);
     const int hist_cells = MODE == MODE_PIVOT ? kct::kLeafCells : 0;
     // compressed pair-level rows: only where a pair level exists (t >= 4)
-    const int mid_words = (MODE == MODE_ORIENT && p.t >= 4) ? kct::kMidWords : 0;
-    const int per_warp = ((p.dcap + 3) & ~3) + 32 * WPL + kct::kSmallWords + hist_cells +
+    const int mid_words = (MODE == MODE_ORIENT && p.t >= 4) ? kct::mid_words(WPL) : 0;
+    // per-warp S-tier rows only: the CTA tier has no LocalMap (kct::kSmallWords)
+    const int per_warp = ((p.dcap + 3) & ~3) + 32 * WPL + kCtaSmallWords + hist_cells +
                          mid_words + p.nsm_frames * p.fw;
     int *list = reinterpret_cast<int *>(area + warp * per_warp);
     uint32_t *cbuf = area + warp * per_warp + ((p.dcap + 3) & ~3);
     kct::SmallScratch SS;
     SS.srow = cbuf + 32 * WPL;
-    SS.sstk = SS.srow + 32;
-    uint32_t *whist = SS.srow + kct::kSmallWords;
+    SS.sstk = nullptr;  // (unused by the CTA-tier walks)
+    uint32_t *whist = SS.srow + kCtaSmallWords;
     if (mid_words) SS.mrow = whist + hist_cells;  // <= 256-member pair levels
     kct::Frames F;
     F.sm = whist + hist_cells + mid_words;
@@ -467,8 +476,13 @@ __global__ void __launch_bounds__(BLOCK) k_count(CountParams p) {
     ull acc = 0, visits = 0, tasks = 0, work = 0, bytes = 0;
     const bool directed = MODE == MODE_ORIENT || (MODE == MODE_EXTRACT && p.directed_out);
     const int t = p.t;
+    long long pc_walk = 0;
     for (;;) {
         __syncthreads();
+        if (p.prof && tid == 0 && pc_walk) {
+            atomicAdd(&p.prof[kProfCtaWalk], ull(clock64() - pc_walk));
+            pc_walk = 0;
+        }
         if (tid == 0) {
             ull i = p.given_rows ? (blockIdx.x == 0 ? atomicAdd(p.task_counter, 1ull) : ~0ull)
                                  : atomicAdd(p.task_counter, 1ull);
@@ -478,6 +492,7 @@ __global__ void __launch_bounds__(BLOCK) k_count(CountParams p) {
         __syncthreads();
         if (s_task < 0) break;
         int d;
+        const long long pc0 = (p.prof && tid == 0) ? clock64() : 0;
         if (p.given_rows) {
             d = load_given<BLOCK>(p, rows);
         } else {
@@ -513,6 +528,7 @@ __global__ void __launch_bounds__(BLOCK) k_count(CountParams p) {
             continue;
         }
         const ull wt0 = work;  // units -> §8(d) word-ops of this task below
+        const long long pc1 = (p.prof && tid == 0) ? clock64() : 0;
         if (MODE == MODE_ORIENT) {
             orient_task<BLOCK, WPL>(p, rows, d, F, list, cbuf, SS, &s_next, acc, visits, work);
         } else {
@@ -520,6 +536,10 @@ __global__ void __launch_bounds__(BLOCK) k_count(CountParams p) {
                                    s_key, visits, work);
         }
         work = wt0 + (work - wt0) * ull((d + 31) >> 5);
+        if (p.prof && tid == 0) {
+            atomicAdd(&p.prof[kProfCtaBuild], ull(pc1 - pc0));
+            pc_walk = pc1;  // closed at the next task's opening barrier
+        }
     }
     __syncthreads();
     if (MODE == MODE_PIVOT) sink.flush(tid & 31);
@@ -676,11 +696,18 @@ __global__ void __launch_bounds__(BLOCK) k_count_warp(CountParams p) {
         if (i >= ull(p.n_tasks)) break;
         const int32_t task = p.tasks[i];
         const bool need_rows = MODE == MODE_PIVOT || t >= 2;
+        const long long pc0 = (p.prof && lane == 0) ? clock64() : 0;
         const int d = warp_build(p, task, l2g, rows, need_rows, MODE == MODE_ORIENT, bytes, SS,
                                  p.task_w && !p.branch ? p.task_w[i] : -1);
+        if (p.prof && lane == 0) {
+            atomicAdd(&p.prof[kProfWarpBuild], ull(clock64() - pc0));
+            if (d > D) atomicAdd(&p.prof[kProfOvfHist + min((d - 1) >> 5, 63)], 1ull);
+        }
+        const long long pc1 = (p.prof && lane == 0) ? clock64() : 0;
         if (d > D) {  // edge task larger than the warp tier: CTA kernel, next launch
             if (lane == 0) {
                 const ull at = atomicAdd(p.overflow_n, 1ull);
+                atomicMax(p.overflow_n + 6, ull(d));  // sizes the CTA launch (dcap)
                 p.overflow[at] = task;
                 if (p.task_w) p.overflow_w[at] = p.task_w[i];
             }
@@ -777,6 +804,7 @@ __global__ void __launch_bounds__(BLOCK) k_count_warp(CountParams p) {
             }
         }
         work = wt0 + (work - wt0) * ull(W);
+        if (p.prof && lane == 0) atomicAdd(&p.prof[kProfWarpWalk], ull(clock64() - pc1));
         __syncwarp();
     }
     if (GQ && MODE == MODE_PIVOT) {
@@ -788,6 +816,7 @@ __global__ void __launch_bounds__(BLOCK) k_count_warp(CountParams p) {
         }
         for (;;) {
             int slot = -1, done = 0;
+            const long long pq0 = (p.prof && lane == 0) ? clock64() : 0;
             if (lane == 0) {
                 // Poll without the lock; take it with a single try (no
                 // spinning on it: a pusher must never queue behind hundreds
@@ -847,6 +876,8 @@ __global__ void __launch_bounds__(BLOCK) k_count_warp(CountParams p) {
             }
             slot = __shfl_sync(kct::FULL, slot, 0);
             done = __shfl_sync(kct::FULL, done, 0);
+            const long long pq1 = (p.prof && lane == 0) ? clock64() : 0;
+            if (p.prof && lane == 0) atomicAdd(&p.prof[kProfGqIdle], ull(pq1 - pq0));
             if (done) break;
             // L2-coherent loads (__ldcg): this SM's L1 may hold an older item
             // of the same slot
@@ -864,9 +895,11 @@ __global__ void __launch_bounds__(BLOCK) k_count_warp(CountParams p) {
                 atomicAdd(q.ctl + 5, 1);  // pops (diagnostics)
                 q.release();
             }
+            if (p.prof && lane == 0) atomicAdd(&p.prof[kProfGqItems + (kind == 1u)], 1ull);
             if (kind == 1u) {  // compressed S-tier subtree: no rebuild
                 kct::pivot_lanes(SS.srow, h0, s0, npv, t, allk, SS.nstk, SS.ncap, sink, lane,
                                  visits, work);
+                if (p.prof && lane == 0) atomicAdd(&p.prof[kProfGqWalk], ull(clock64() - pq1));
                 if (lane == 0) {
                     atomicAdd(q.ctl + 2, 1);
                     atomicSub(q.ctl + 3, 1);
@@ -892,6 +925,7 @@ __global__ void __launch_bounds__(BLOCK) k_count_warp(CountParams p) {
                                      visits, work);
             }
             work = wt0 + (work - wt0) * ull(W);
+            if (p.prof && lane == 0) atomicAdd(&p.prof[kProfGqWalk], ull(clock64() - pq1));
             if (lane == 0) {
                 atomicAdd(q.ctl + 2, 1);
                 atomicSub(q.ctl + 3, 1);
@@ -1064,6 +1098,36 @@ inline int grid_1d(int64_t n, int sms) {
 // stream of the current library call: DevBuf allocations are stream-ordered on it
 thread_local cudaStream_t tl_stream = nullptr;
 thread_local int tl_launches = 0;  // counting-kernel launches of the current call
+// KC_TIMING=1: device time of every counting launch (events on its stream),
+// printed to stderr at the end of kc_count -- a launch list without ncu
+struct LaunchTimer {
+    const char *what;
+    int64_t n_tasks;
+    int grid;
+    cudaEvent_t a, b;
+};
+thread_local std::vector<LaunchTimer> tl_timers;
+inline bool timing_on() {
+    static const bool on = [] {
+        const char *e = getenv("KC_TIMING");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+inline cudaEvent_t timer_begin(cudaStream_t s) {
+    if (!timing_on()) return nullptr;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, s);
+    return e;
+}
+inline void timer_end(cudaEvent_t a, cudaStream_t s, const char *what, int64_t n, int grid) {
+    if (!a) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, s);
+    tl_timers.push_back({what, n, grid, a, e});
+}
 struct StreamScope {
     cudaStream_t prev;
     explicit StreamScope(cudaStream_t s) : prev(tl_stream) { tl_stream = s; }
@@ -1091,8 +1155,9 @@ struct DevBuf {
 // persistent queue balanced).  Returns the count.
 int64_t build_tasks(kc_graph *g, int scheme, int64_t lo, int64_t hi, int min_d, DevBuf &out,
                     uint32_t big_thr, int64_t *n_big, const uint8_t *vsel = nullptr,
-                    uint32_t mid_thr = 0, int64_t *n_mid = nullptr) {
+                    uint32_t mid_thr = 0, int64_t *n_mid = nullptr, uint32_t *max_key = nullptr) {
     if (n_mid) *n_mid = 0;
+    if (max_key) *max_key = 0;
     const int64_t N = scheme == KC_SCHEME_EDGE ? g->m_dir : g->n;
     *n_big = 0;
     if (N == 0) return 0;
@@ -1149,6 +1214,8 @@ int64_t build_tasks(kc_graph *g, int scheme, int64_t lo, int64_t hi, int min_d, 
         int32_t nb[2] = {0, 0};
         KC_CUDA(cudaMemcpyAsync(nb, cnt.as<int32_t>() + 1, 8, cudaMemcpyDeviceToHost,
                                 g->stream));
+        if (max_key)  // keys sorted descending: the largest task's locals (bound)
+            KC_CUDA(cudaMemcpyAsync(max_key, key.p, 4, cudaMemcpyDeviceToHost, g->stream));
         KC_CUDA(cudaStreamSynchronize(g->stream));
         *n_big = nb[0];
         if (n_mid) *n_mid = nb[1];
@@ -1164,7 +1231,7 @@ constexpr int kSmidSlots = 1024;  // %smid can exceed the SM count
 // the overflow count, then the subtree queue's control words (8 ints)
 constexpr int kOutGq = 8 + kSmidSlots + 12;
 constexpr int kOutWords = kOutGq + 4;
-constexpr int kSmemMax = 220 * 1024;
+constexpr int kSmemMax = 225 * 1024;  // of 227 KB per block (static smem < 2 KB)
 constexpr int kSmemTarget = 100 * 1024;  // aim for >= 2 resident CTAs per SM
 
 // DFS frames a warp can touch: orient frames 1..t-3 (frame t-2 is scored in
@@ -1180,20 +1247,26 @@ typedef std::vector<std::unique_ptr<DevBuf>> Keep;
 // launched on (DevBuf(bytes, stream)), so a kernel on the aux stream never
 // waits for, nor races with, the graph stream's allocations and frees.
 
-template <int MODE, int WPL>
-void launch_wpl(kc_graph *g, CountParams &p, int grid_override, Keep &keep,
-                cudaStream_t stream) {
-    constexpr int NW = kBlock / 32;
+// shared-memory plan of the CTA-tier kernel for one block size
+struct CtaPlan {
+    size_t smem = 0;
+    int nsm = 0, rows_in_smem = 0, per_sm = 0;
+    const void *kern = nullptr;
+};
+
+template <int MODE, int WPL, int BLOCK>
+CtaPlan plan_cta(const CountParams &p) {
+    constexpr int NW = BLOCK / 32;
+    CtaPlan pl;
     const size_t hist_words = MODE == MODE_PIVOT ? kct::kLeafCells : 0;
     const size_t dpad = size_t((p.dcap + 3) & ~3);
     const size_t l2g_bytes = 4 * dpad;
     const size_t rows_words = (size_t(p.dcap) * row_stride(p.wcap) + 3) & ~size_t(3);
-    p.fw = MODE == MODE_PIVOT ? 64 * WPL + 4 : 32 * WPL + 4;
     const int need = frames_needed(MODE, p.t, p.dcap);
     auto area_words = [&](int nsm) {
         size_t w = (MODE == MODE_PIVOT ? 64 * WPL + kStealCap * (32 * WPL + 4) : 0) +
-                   size_t(NW) * (dpad + 32 * WPL + kct::kSmallWords + hist_words +
-                                 (MODE == MODE_ORIENT && p.t >= 4 ? kct::kMidWords : 0) +
+                   size_t(NW) * (dpad + 32 * WPL + kCtaSmallWords + hist_words +
+                                 (MODE == MODE_ORIENT && p.t >= 4 ? kct::mid_words(WPL) : 0) +
                                  size_t(nsm) * p.fw);
         if (p.scheme == KC_SCHEME_EDGE) w = std::max(w, dpad);
         if (MODE != MODE_PIVOT) {
@@ -1208,19 +1281,32 @@ void launch_wpl(kc_graph *g, CountParams &p, int grid_override, Keep &keep,
     auto total = [&](int ns, bool rows_smem) {
         return l2g_bytes + 4 * area_words(ns) + (rows_smem ? 4 * rows_words : 0) + 64;
     };
-    p.rows_in_smem = total(std::min(nsm, 4), true) <= size_t(kSmemMax);
-    while (nsm > 4 && total(nsm, p.rows_in_smem) > size_t(kSmemTarget)) nsm >>= 1;
-    while (nsm > 1 && total(nsm, p.rows_in_smem) > size_t(kSmemMax)) --nsm;
-    p.nsm_frames = nsm;
-    const size_t smem = total(nsm, p.rows_in_smem);
-    KC_REQUIRE(smem <= size_t(kSmemMax), KC_ENOMEM, "per-task scratch exceeds shared memory");
-    auto kern = (MODE == MODE_PIVOT && p.use_gq) ? k_count<kBlock, MODE, WPL, true>
-                                                 : k_count<kBlock, MODE, WPL, false>;
-    KC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    int per_sm = 0;
-    KC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBlock, smem));
-    KC_REQUIRE(per_sm > 0, KC_ECUDA, "count kernel cannot be resident");
-    int grid = grid_override > 0 ? grid_override : per_sm * g->num_sms;
+    pl.rows_in_smem = total(std::min(nsm, 4), true) <= size_t(kSmemMax);
+    while (nsm > 4 && total(nsm, pl.rows_in_smem) > size_t(kSmemTarget)) nsm >>= 1;
+    while (nsm > 1 && total(nsm, pl.rows_in_smem) > size_t(kSmemMax)) --nsm;
+    pl.nsm = nsm;
+    pl.smem = total(nsm, pl.rows_in_smem);
+    if (pl.smem > size_t(kSmemMax)) return pl;  // per_sm = 0: not launchable
+    auto kern = (MODE == MODE_PIVOT && p.use_gq) ? k_count<BLOCK, MODE, WPL, true>
+                                                 : k_count<BLOCK, MODE, WPL, false>;
+    KC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(pl.smem)));
+    KC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pl.per_sm, kern, BLOCK, pl.smem));
+    pl.kern = reinterpret_cast<const void *>(kern);
+    return pl;
+}
+
+template <int MODE, int WPL, int BLOCK>
+void launch_cta(kc_graph *g, CountParams &p, const CtaPlan &pl, int grid_override, Keep &keep,
+                cudaStream_t stream) {
+    constexpr int NW = BLOCK / 32;
+    KC_REQUIRE(pl.smem <= size_t(kSmemMax), KC_ENOMEM, "per-task scratch exceeds shared memory");
+    KC_REQUIRE(pl.per_sm > 0, KC_ECUDA, "count kernel cannot be resident");
+    const size_t rows_words = (size_t(p.dcap) * row_stride(p.wcap) + 3) & ~size_t(3);
+    const int need = frames_needed(MODE, p.t, p.dcap);
+    p.rows_in_smem = pl.rows_in_smem;
+    p.nsm_frames = pl.nsm;
+    int grid = grid_override > 0 ? grid_override : pl.per_sm * g->num_sms;
     if (p.n_tasks > 0 && int64_t(grid) > p.n_tasks && !grid_override) grid = int(p.n_tasks);
     if (grid < 1) grid = 1;
     if (!p.rows_in_smem) {
@@ -1230,14 +1316,49 @@ void launch_wpl(kc_graph *g, CountParams &p, int grid_override, Keep &keep,
     }
     p.frames_global = nullptr;
     p.frames_slot = 0;
-    if (MODE != MODE_EXTRACT && need > nsm) {
-        p.frames_slot = int64_t(need - nsm) * p.fw;
+    if (MODE != MODE_EXTRACT && need > pl.nsm) {
+        p.frames_slot = int64_t(need - pl.nsm) * p.fw;
         keep.emplace_back(new DevBuf(4 * size_t(p.frames_slot) * size_t(grid) * NW, stream));
         p.frames_global = keep.back()->as<uint32_t>();
     }
-    kern<<<grid, kBlock, smem, stream>>>(p);
+    auto kern = (MODE == MODE_PIVOT && p.use_gq) ? k_count<BLOCK, MODE, WPL, true>
+                                                 : k_count<BLOCK, MODE, WPL, false>;
+    cudaEvent_t t0 = timer_begin(stream);
+    kern<<<grid, BLOCK, pl.smem, stream>>>(p);
     KC_CUDA(cudaGetLastError());
+    timer_end(t0, stream,
+              MODE == MODE_PIVOT ? "cta/pivot"
+                                 : (BLOCK == 128 ? "cta/orient" : BLOCK == 256 ? "cta/orient-256"
+                                                                               : "cta/orient-512"),
+              p.n_tasks, grid);
     ++tl_launches;
+}
+
+// CTA tier.  Orientation with one word per lane (d <= 1024): the block size
+// (4, 8 or 16 warps sharing one task's bit matrix) that keeps the most warps
+// resident per SM -- with big matrices (RMAT-22: 964 locals, 119 KB) a
+// 4-warp CTA leaves the SM at one CTA, 4 warps.
+template <int MODE, int WPL>
+void launch_wpl(kc_graph *g, CountParams &p, int grid_override, Keep &keep,
+                cudaStream_t stream) {
+    p.fw = MODE == MODE_PIVOT ? 64 * WPL + 4 : 32 * WPL + 4;
+    const CtaPlan p128 = plan_cta<MODE, WPL, 128>(p);
+    if constexpr (MODE == MODE_ORIENT && WPL == 1) {
+        if (grid_override <= 0 && p.n_tasks > int64_t(g->num_sms)) {
+            const CtaPlan p256 = plan_cta<MODE, WPL, 256>(p);
+            const CtaPlan p512 = plan_cta<MODE, WPL, 512>(p);
+            const int w128 = p128.per_sm * 4, w256 = p256.per_sm * 8, w512 = p512.per_sm * 16;
+            if (w512 > w256 && w512 > w128) {
+                launch_cta<MODE, WPL, 512>(g, p, p512, grid_override, keep, stream);
+                return;
+            }
+            if (w256 > w128) {
+                launch_cta<MODE, WPL, 256>(g, p, p256, grid_override, keep, stream);
+                return;
+            }
+        }
+    }
+    launch_cta<MODE, WPL, 128>(g, p, p128, grid_override, keep, stream);
 }
 
 // warp-per-task kernel for tasks with at most kWarpD locals
@@ -1282,8 +1403,17 @@ void launch_warp(kc_graph *g, CountParams &p, Keep &keep, cudaStream_t stream) {
         keep.emplace_back(new DevBuf(4 * size_t(p.frames_slot) * size_t(grid) * NW, stream));
         p.frames_global = keep.back()->as<uint32_t>();
     }
+    cudaEvent_t t0 = timer_begin(stream);
     kern<<<grid, kBlock, smem, stream>>>(p);
     KC_CUDA(cudaGetLastError());
+    timer_end(t0, stream,
+              MODE == MODE_PIVOT ? (p.roots_only ? "warp/pivot-roots"
+                                    : p.branch   ? "warp/pivot-branches"
+                                                 : "warp/pivot")
+                                 : (p.task_w ? "warp/orient-triples"
+                                    : p.split ? "warp/orient-items"
+                                              : "warp/orient"),
+              p.n_tasks, grid);
     ++tl_launches;
 }
 
@@ -1334,6 +1464,7 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
     kc_device_guard guard(g->device);
     StreamScope scope(g->stream);
     tl_launches = 0;
+    tl_timers.clear();
 
     int64_t all = kc_task_count(g, a->scheme);
     int64_t lo = a->task_lo < 0 ? 0 : a->task_lo;
@@ -1355,6 +1486,7 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
     }
     DevBuf tasks;
     int64_t n_big = 0, n_mid = 0;
+    uint32_t max_task_d = 0;  // largest task's locals (exact for vertex and edge keys)
     // pivot: warp-tier tasks above kPivotSplitD locals are split at the root
     static const int pivot_split_d = [] {
         const char *e = getenv("KC_PIVOT_SPLIT");
@@ -1364,10 +1496,11 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
                         pivot_split_d < kWarpD;
     const int64_t n_tasks =
         build_tasks(g, a->scheme, lo, hi, min_d, tasks, split ? kSplitD : kWarpD, &n_big, nullptr,
-                    uint32_t(pivot_split_d), psplit ? &n_mid : nullptr);
+                    uint32_t(pivot_split_d), psplit ? &n_mid : nullptr, &max_task_d);
     const int64_t n_split = psplit ? std::max<int64_t>(n_mid - n_big, 0) : 0;
     DevBuf items;
     int64_t n_items = 0, n_items_big = 0;
+    uint32_t max_item_d = 0;
     if (split && n_big > 0) {
         DevBuf vsel(size_t(g->n > 0 ? g->n : 1));
         KC_CUDA(cudaMemsetAsync(vsel.p, 0, size_t(g->n > 0 ? g->n : 1), g->stream));
@@ -1375,7 +1508,7 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
                                                                         vsel.as<uint8_t>());
         KC_CUDA(cudaGetLastError());
         n_items = build_tasks(g, KC_SCHEME_EDGE, 0, g->m_dir, 0, items, kWarpD, &n_items_big,
-                              vsel.as<uint8_t>());
+                              vsel.as<uint8_t>(), 0, nullptr, &max_item_d);
     }
 
     DevBuf outs(8 * size_t(kOutWords));
@@ -1407,6 +1540,11 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
     p.visits_per_sm = o + 8;
     p.word_ops = o + 8 + kSmidSlots;
     p.ext_bytes = o + 9 + kSmidSlots;
+    DevBuf prof(timing_on() ? 8 * size_t(kProfWords) : 8);
+    if (timing_on()) {
+        KC_CUDA(cudaMemsetAsync(prof.p, 0, 8 * size_t(kProfWords), g->stream));
+        p.prof = prof.as<ull>();
+    }
 
     cudaEvent_t e0, e1, e_fork, e_join;
     KC_CUDA(cudaEventCreate(&e0));
@@ -1466,6 +1604,8 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
             b.split = 1;
             b.tasks = items.as<int32_t>();
             b.n_tasks = n_items_big;
+            b.dcap = int(std::max<uint32_t>(std::min<uint32_t>(max_item_d, uint32_t(p.dcap)), 1u));
+            b.wcap = (b.dcap + 31) / 32;
             b.task_counter = o + 8 + kSmidSlots + 6;
             launch<MODE_ORIENT>(g, b, 0, keep, g->stream);
         }
@@ -1528,6 +1668,8 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
         if (n_big > 0) {
             CountParams b = p;
             b.n_tasks = n_big;
+            b.dcap = int(std::max<uint32_t>(std::min<uint32_t>(max_task_d, uint32_t(p.dcap)), 1u));
+            b.wcap = (b.dcap + 31) / 32;
             if (pivot) launch<MODE_PIVOT>(g, b, 0, keep, g->stream);
             else launch<MODE_ORIENT>(g, b, 0, keep, g->stream);
         }
@@ -1597,9 +1739,11 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
         }
     }
     if (edge_like) {
-        ull n_ovf = 0;
-        KC_CUDA(cudaMemcpyAsync(&n_ovf, p.overflow_n, 8, cudaMemcpyDeviceToHost, g->stream));
+        ull ovf_hdr[7] = {0, 0, 0, 0, 0, 0, 0};
+        KC_CUDA(cudaMemcpyAsync(ovf_hdr, p.overflow_n, sizeof(ovf_hdr), cudaMemcpyDeviceToHost,
+                                g->stream));
         KC_CUDA(cudaStreamSynchronize(g->stream));
+        const ull n_ovf = ovf_hdr[0];
         if (n_ovf > 0) {
             // in split mode only triples can overflow (items and roots are
             // routed by exact size); elsewhere only plain edge tasks
@@ -1610,6 +1754,10 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
             b.task_w = split ? ovf_w.as<int32_t>() : nullptr;
             b.tasks = ovf.as<int32_t>();
             b.n_tasks = int64_t(n_ovf);
+            // shared memory sized for the largest overflow task, not d_max:
+            // RMAT-22 k=7 overflow triples have <= 416 locals against d_max 964
+            b.dcap = int(std::max<ull>(std::min<ull>(ovf_hdr[6], ull(p.dcap)), 1ull));
+            b.wcap = (b.dcap + 31) / 32;
             b.task_counter = o + 8 + kSmidSlots + 4;
             if (pivot) launch<MODE_PIVOT>(g, b, 0, keep, g->stream);
             else launch<MODE_ORIENT>(g, b, 0, keep, g->stream);
@@ -1621,6 +1769,34 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
     KC_CUDA(cudaEventSynchronize(e1));
     float ms = 0;
     KC_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    for (auto &lt : tl_timers) {
+        float lms = 0;
+        cudaEventElapsedTime(&lms, lt.a, lt.b);
+        fprintf(stderr, "[kc_timing] %-22s tasks=%-10lld grid=%-5d %10.3f ms\n", lt.what,
+                (long long)lt.n_tasks, lt.grid, lms);
+        cudaEventDestroy(lt.a);
+        cudaEventDestroy(lt.b);
+    }
+    if (!tl_timers.empty()) {
+        fprintf(stderr, "[kc_timing] count phase %10.3f ms\n", ms);
+        std::vector<ull> hp(kProfWords);
+        KC_CUDA(cudaMemcpy(hp.data(), prof.p, 8 * hp.size(), cudaMemcpyDeviceToHost));
+        fprintf(stderr,
+                "[kc_timing] cycles: cta build %.3e walk %.3e (per CTA, thread 0); warp build "
+                "%.3e walk %.3e (summed over warps)\n",
+                double(hp[kProfCtaBuild]), double(hp[kProfCtaWalk]), double(hp[kProfWarpBuild]),
+                double(hp[kProfWarpWalk]));
+        fprintf(stderr,
+                "[kc_timing] subtree queue: idle %.3e walk %.3e cycles (summed over warps), "
+                "items id-list %llu compressed %llu\n",
+                double(hp[kProfGqIdle]), double(hp[kProfGqWalk]), hp[kProfGqItems],
+                hp[kProfGqItems + 1]);
+        fprintf(stderr, "[kc_timing] overflow sizes (32-local buckets):");
+        for (int b = 0; b < 64; ++b)
+            if (hp[kProfOvfHist + b]) fprintf(stderr, " %d:%llu", (b + 1) * 32, hp[kProfOvfHist + b]);
+        fprintf(stderr, "\n");
+    }
+    tl_timers.clear();
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     cudaEventDestroy(e_fork);

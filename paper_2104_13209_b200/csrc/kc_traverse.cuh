@@ -400,55 +400,80 @@ __device__ __forceinline__ void score_pairs8(const uint32_t *__restrict__ rows, 
 // Pair level of a wide task (rows of W > 4 words, the CTA tier) whose set X
 // has 33..256 members: relabel X's members 0..n-1 (ascending local id) and
 // compress their rows restricted to X into 16- or 32-byte rows (mrow), then
-// run the four- / eight-word pair loop over them.  Member j of row i is found by
-// walking the set bits of X & row i word by word, its new index being the
-// count of X's members below it (per-word prefix counts) -- the work is one
-// step per (i, j) edge inside X, the pair count the loop would walk anyway.
+// run the four- / eight-word pair loop over them.  Compression is a parallel
+// bit extract per word (Hacker's Delight 7-4 "compress": five shift/mask steps
+// whose masks depend only on X's word, built once per set), the extracted
+// pieces funnelled into the output row at the running offset -- a fixed cost
+// per (member, word) with no divergence between lanes (the earlier per-bit
+// loop ran at ~2 active lanes: ncu, profiles/r2b_ncu_cta_orient_rmat22.md).
 // Counts and visits are order-free sums, hence unchanged.
+__device__ __forceinline__ void compress_masks(uint32_t m, uint32_t (&mv)[5]) {
+    uint32_t mk = ~m << 1;
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+        uint32_t mp = mk ^ (mk << 1);
+        mp ^= mp << 2;
+        mp ^= mp << 4;
+        mp ^= mp << 8;
+        mp ^= mp << 16;
+        mv[i] = mp & m;
+        m = (m ^ mv[i]) | (mv[i] >> (1 << i));
+        mk &= ~mp;
+    }
+}
+
 template <int WPL>
 __device__ __forceinline__ void score_pairs_mid(const uint32_t *__restrict__ rows, int RS, int W,
                                                 const Set<WPL> &X, int *list, uint32_t *cbuf,
                                                 uint32_t *mrow, int lane, ull &acc, ull &visits,
                                                 ull &work) {
+    (void)cbuf;
     const int n = compact<WPL>(X, list, lane, W);
-    uint32_t *cum = mrow + 256 * 8;  // exclusive prefix popcount of X's words
-    int carry = 0;
+    // per word w of X: [X_w, popc(X_w), mv0..mv4, -] (two 16-byte loads)
+    uint32_t *tab = mrow + 256 * 8;
 #pragma unroll
     for (int p = 0; p < WPL; ++p) {
-        const int c = __popc(X.w[p]);
-        int incl = c;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(FULL, incl, o);
-            if (lane >= o) incl += y;
+        const int w = p * 32 + lane;
+        if (w < W) {
+            uint32_t mv[5];
+            compress_masks(X.w[p], mv);
+            *reinterpret_cast<uint4 *>(tab + w * 8) =
+                make_uint4(X.w[p], uint32_t(__popc(X.w[p])), mv[0], mv[1]);
+            *reinterpret_cast<uint4 *>(tab + w * 8 + 4) = make_uint4(mv[2], mv[3], mv[4], 0u);
         }
-        cbuf[p * 32 + lane] = X.w[p];
-        cum[p * 32 + lane] = uint32_t(carry + incl - c);
-        carry += __shfl_sync(FULL, incl, 31);
     }
     __syncwarp();
     const int RSM = n <= 128 ? 4 : 8;  // compressed row stride (words)
     for (int i = lane; i < n; i += 32) {
         const uint32_t *ri = rows + list[i] * RS;
-        uint32_t cr[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+        uint32_t *out = mrow + i * RSM;
+        uint32_t lo = 0u, hi = 0u;
+        int fill = 0, q = 0;
         for (int w = 0; w < W; ++w) {
-            const uint32_t xw = cbuf[w];
-            uint32_t m = xw & ri[w];
-            if (!m) continue;
-            const int base = int(cum[w]);
-            while (m) {
-                const int b = __ffs(m) - 1;
-                m &= m - 1u;
-                const int j = base + __popc(xw & ((1u << b) - 1u));
-                const uint32_t bit = 1u << (j & 31);
-                const int q = j >> 5;
-#pragma unroll
-                for (int k = 0; k < 8; ++k) cr[k] |= q == k ? bit : 0u;
+            const uint4 a = *reinterpret_cast<const uint4 *>(tab + w * 8);
+            if (a.x == 0u) continue;  // uniform: depends on X only
+            uint32_t x = ri[w] & a.x;
+            if (a.x != FULL) {
+                const uint4 b = *reinterpret_cast<const uint4 *>(tab + w * 8 + 4);
+                uint32_t t;
+                t = x & a.z;  x = (x ^ t) | (t >> 1);
+                t = x & a.w;  x = (x ^ t) | (t >> 2);
+                t = x & b.x;  x = (x ^ t) | (t >> 4);
+                t = x & b.y;  x = (x ^ t) | (t >> 8);
+                t = x & b.z;  x = (x ^ t) | (t >> 16);
+            }
+            lo |= x << fill;
+            hi |= __funnelshift_l(x, 0u, fill);  // bits of x shifted past bit 31
+            fill += int(a.y);
+            if (fill >= 32) {  // uniform
+                out[q++] = lo;
+                lo = hi;
+                hi = 0u;
+                fill -= 32;
             }
         }
-        *reinterpret_cast<uint4 *>(mrow + i * RSM) = make_uint4(cr[0], cr[1], cr[2], cr[3]);
-        if (RSM == 8)
-            *reinterpret_cast<uint4 *>(mrow + i * RSM + 4) = make_uint4(cr[4], cr[5], cr[6], cr[7]);
+        if (fill > 0) out[q++] = lo;
+        while (q < RSM) out[q++] = 0u;
     }
     __syncwarp();
     if (RSM == 8) {
@@ -1323,9 +1348,10 @@ struct SmallScratch {
     uint32_t *sstk;  // kMapWords words: LocalMap storage
     uint2 *nstk = nullptr;  // pivot per-lane node stack (warp tier), nullptr: uniform walks
     int ncap = 0;
-    uint32_t *mrow = nullptr;  // kMidWords: compressed <= 128-member pair level (CTA tier)
+    uint32_t *mrow = nullptr;  // mid_words(WPL): compressed <= 256-member pair level (CTA tier)
 };
-constexpr int kMidWords = 256 * 8 + 128;  // 256 rows of 8 words + per-word prefix counts
+// 256 rows of 8 words + the per-word compress table of a set (8 words per word)
+constexpr int mid_words(int wpl) { return 256 * 8 + 8 * 32 * wpl; }
 constexpr int kNodeCap = 512;  // pivot_lanes stack capacity (nodes of 2 words)
 constexpr int kMapSlots = 256;
 constexpr int kMapWords = kMapSlots + kMapSlots / 4;

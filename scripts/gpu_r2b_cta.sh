@@ -1,0 +1,16 @@
+#!/bin/bash
+# CTA tier sized by the actual max locals + block size by occupancy: GPU
+# parity suite, then RMAT-22 k=7 1/64 slice, RMAT-20 k=7, RMAT-18 k=7 (KC_TIMING)
+mkdir -p gpurun_out
+export PYTHONPATH=$PWD KC_GRAPH_CACHE=/tmp/kc_graphs
+timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/r2b_cta_tests.log 2>&1
+echo "rc=$?" >> gpurun_out/r2b_cta_tests.log
+export KC_TIMING=1
+O=gpurun_out/r2b_cta.log
+: > $O
+timeout 300 python scripts/shard_probe.py --workload rmat22 --k 7 --algo orient --scheme vertex --world 64 --ranks 0 >> $O 2>&1
+echo "rc=$?" >> $O
+timeout 300 python scripts/explore.py --workload rmat20 --k 7 --algo orient --scheme vertex --criterion degeneracy --reps 1 >> $O 2>&1
+echo "rc=$?" >> $O
+timeout 300 python scripts/explore.py --workload rmat18 --k 7 --algo orient --scheme vertex --criterion degeneracy --reps 2 >> $O 2>&1
+echo "rc=$?" >> $O

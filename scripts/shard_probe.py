@@ -1,0 +1,59 @@
+"""Time single shards of a big run (estimate the whole run from a slice).
+
+    python scripts/shard_probe.py --workload rmat22 --k 7 --algo orient \
+        --scheme vertex --world 16 --ranks 0 7 15
+
+Each listed rank's root range (kc_shard_ranges, cost-balanced) is counted
+alone with device_count_raw; one JSON line per shard with its device ms,
+visits and raw limbs.  With KC_TIMING=1 the library prints per-launch times.
+"""
+
+import argparse
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np  # noqa: E402
+import paper_2104_13209_b200 as kc  # noqa: E402
+from paper_2104_13209_b200.orientation import rank_and_orient  # noqa: E402
+from paper_2104_13209_b200.scheduler import device_count_raw  # noqa: E402
+from paper_2104_13209_b200.shard import shard_ranges  # noqa: E402
+
+from explore import cached_edges  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--workload", default="rmat22")
+    ap.add_argument("--k", type=int, default=7)
+    ap.add_argument("--algo", default="orient")
+    ap.add_argument("--scheme", default="vertex")
+    ap.add_argument("--criterion", default="degeneracy")
+    ap.add_argument("--world", type=int, default=16)
+    ap.add_argument("--ranks", type=int, nargs="+", default=[0])
+    a = ap.parse_args()
+    g = kc.from_edges(cached_edges(a.workload))
+    cfg = kc.RunConfig(k=a.k, algorithm=a.algo, scheme=a.scheme, criterion=a.criterion)
+    t = time.perf_counter()
+    og = rank_and_orient(g, a.criterion)
+    orient_s = time.perf_counter() - t
+    ranges = shard_ranges(og, cfg, a.world)
+    print(json.dumps({"workload": a.workload, "n": g.n, "m": g.m, "d_max": og.d_max,
+                      "orient_s": round(orient_s, 3), "world": a.world,
+                      "ranges": ranges}), flush=True)
+    for r in a.ranks:
+        lo, hi = ranges[r]
+        t = time.perf_counter()
+        raw = device_count_raw(og, cfg, lo, hi)
+        print(json.dumps({"rank": r, "lo": lo, "hi": hi, "wall_s": round(time.perf_counter() - t, 3),
+                          "kernel_ms": raw.count_ms, "visits": int(raw.visits),
+                          "limbs": [int(x) for x in raw.limbs], "word_ops": int(raw.word_ops),
+                          "hist_sum": int(np.asarray(raw.hist, dtype=np.uint64).sum()) if raw.hist is not None else 0}),
+              flush=True)
+
+
+if __name__ == "__main__":
+    main()
