@@ -88,6 +88,12 @@ struct CountParams {
     ull *visits_per_sm;
     ull *tasks_run;
     ull *prof;  // KC_TIMING diagnostics (nullptr: off): see kProf* below
+    // pivot bounded walks (kct::Spill): items out, and (spill rounds) items in
+    kct::Spill spill;
+    int use_spill;
+    int spill_budget;
+    const uint32_t *in_buf;  // spill round: task i is the item at in_buf + in_off[i]
+    const uint32_t *in_off;
 };
 // prof words: CTA tier build / walk cycles (thread 0), warp tier build / walk
 // cycles (lane 0, summed over warps), then a histogram of overflow task sizes
@@ -149,6 +155,10 @@ __device__ __forceinline__ bool gl_contains(const int32_t *__restrict__ a, int n
     return lo < n && __ldg(a + lo) == x;
 }
 
+template <int BLOCK>
+__device__ void rows_from_locals(const CountParams &p, const int32_t *l2g, int d, uint32_t *rows,
+                                 int32_t *scratch, bool directed, ull &bytes);
+
 // Returns d (number of locals); fills l2g and (when t >= 2 or pivot) rows.
 // scratch must hold >= dcap int32 (used for the edge scheme's second list).
 template <int BLOCK>
@@ -190,6 +200,18 @@ __device__ int build_task(const CountParams &p, int32_t task, int32_t *l2g, uint
     }
     __syncthreads();
     if (!need_rows || d == 0) return d;
+    rows_from_locals<BLOCK>(p, l2g, d, rows, scratch, directed, bytes);
+    return d;
+}
+
+// bit matrix of the sub-graph induced by the sorted vertices l2g[0..d)
+// (bitgraph.py:89-111: bit j of row i <=> arc l2g[i] -> l2g[j], or either
+// arc when undirected); whole block, ends with a barrier
+template <int BLOCK>
+__device__ void rows_from_locals(const CountParams &p, const int32_t *l2g, int d, uint32_t *rows,
+                                 int32_t *scratch, bool directed, ull &bytes) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int NW = BLOCK / 32;
     const int W = (d + 31) >> 5, RS = row_stride(W);
     for (int i = tid; i < d * RS; i += BLOCK) rows[i] = 0u;
     // orientation: global id -> local index by open addressing over H >= 2d
@@ -240,7 +262,6 @@ __device__ int build_task(const CountParams &p, int32_t task, int32_t *l2g, uint
         }
     }
     __syncthreads();
-    return d;
 }
 
 // engine entry: load a host-provided matrix instead of extracting
@@ -345,11 +366,13 @@ __device__ void pivot_task(const CountParams &p, const uint32_t *rows, int d, ui
                            uint32_t *P0, const kct::Frames &F, int *list,
                            const kct::SmallScratch &SS, const kct::PivotLeafSink &sink,
                            const kct::StealStack &q, int *s_next, int *s_piv0, ull *s_key,
-                           ull &visits, ull &work) {
+                           ull &visits, ull &work, int s0 = 0, int npv0 = 0) {
     constexpr int NW = BLOCK / 32;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int W = (d + 31) >> 5, RS = row_stride(W);
     // root frame (engine_pivot.py:133-136): S0 = all locals, pivot = argmax |row c|
+    // (a spilled item: S0 = all members of the item's set, at depth s0 with
+    // npv0 pivots)
     for (int w = tid; w < 32 * WPL; w += BLOCK) {
         const int lo = w << 5;
         S0[w] = lo >= d ? 0u : (lo + 32 <= d ? kct::FULL : ((1u << (d - lo)) - 1u));
@@ -392,7 +415,7 @@ __device__ void pivot_task(const CountParams &p, const uint32_t *rows, int d, ui
         if (v >= d) break;
         if (!((P0[v >> 5] >> (v & 31)) & 1u)) continue;
         kct::pivot_subtree<WPL>(rows, RS, W, p.t, p.all_k != 0, v, piv0, S0, P0, F, list, SS,
-                                sink, visits, work, &q);
+                                sink, visits, work, &q, s0, npv0);
     }
     kct::pivot_steal_loop<WPL>(rows, RS, W, p.t, p.all_k != 0, F, list, SS, sink, q, visits, work);
 }
@@ -439,8 +462,10 @@ __global__ void __launch_bounds__(BLOCK) k_count(CountParams p) {
     // compressed pair-level rows: only where a pair level exists (t >= 4)
     const int mid_words = (MODE == MODE_ORIENT && p.t >= 4) ? kct::mid_words(WPL) : 0;
     // per-warp S-tier rows only: the CTA tier has no LocalMap (kct::kSmallWords)
+    // pivot: per-lane S-tier walks need a node stack per warp
+    const int node_words = MODE == MODE_PIVOT ? 2 * kct::kNodeCap : 0;
     const int per_warp = ((p.dcap + 3) & ~3) + 32 * WPL + kCtaSmallWords + hist_cells +
-                         mid_words + p.nsm_frames * p.fw;
+                         mid_words + node_words + p.nsm_frames * p.fw;
     int *list = reinterpret_cast<int *>(area + warp * per_warp);
     uint32_t *cbuf = area + warp * per_warp + ((p.dcap + 3) & ~3);
     kct::SmallScratch SS;
@@ -448,13 +473,18 @@ __global__ void __launch_bounds__(BLOCK) k_count(CountParams p) {
     SS.sstk = nullptr;  // (unused by the CTA-tier walks)
     uint32_t *whist = SS.srow + kCtaSmallWords;
     if (mid_words) SS.mrow = whist + hist_cells;  // <= 256-member pair levels
+    if (node_words) {
+        SS.nstk = reinterpret_cast<uint2 *>(whist + hist_cells + mid_words);
+        SS.ncap = kct::kNodeCap;
+    }
     kct::Frames F;
-    F.sm = whist + hist_cells + mid_words;
+    F.sm = whist + hist_cells + mid_words + node_words;
     F.nsm = p.nsm_frames;
     F.fw = p.fw;
     F.gm = p.frames_global ? p.frames_global + (int64_t(blockIdx.x) * NW + warp) * p.frames_slot
                            : nullptr;
-    __shared__ int s_hc[2 * NW];
+    __shared__ int s_hc[4 * NW];
+    __shared__ int s_spill;  // bounded walks: set once a warp of the task is over budget
     kct::PivotLeafSink sink;
     sink.whist = whist;
     sink.g_hist = p.hist;
@@ -462,7 +492,11 @@ __global__ void __launch_bounds__(BLOCK) k_count(CountParams p) {
     sink.gq = (GQ && MODE == MODE_PIVOT) ? &p.gq : nullptr;  // compile-time off when !GQ
     sink.eager = true;  // CTA tier
     sink.l2g = l2g;
-    sink.hc = s_hc + 2 * warp;
+    sink.hc = s_hc + 4 * warp;
+    if (MODE == MODE_PIVOT && p.use_spill) {
+        sink.sp = &p.spill;
+        sink.cta_flag = &s_spill;
+    }
     sink.push_min = p.gq_push_min;
     sink.cooldown = p.gq_cooldown;
     sink.room_min = p.gq_room;
@@ -488,13 +522,26 @@ __global__ void __launch_bounds__(BLOCK) k_count(CountParams p) {
                                  : atomicAdd(p.task_counter, 1ull);
             s_task = i < ull(p.n_tasks) ? int(i) : -1;
             s_next = 0;
+            s_spill = 0;
         }
+        if (sink.sp) sink.set_budget(p.spill_budget, tid & 31);
         __syncthreads();
         if (s_task < 0) break;
         int d;
+        int it_s = 0, it_npv = 0;  // spill round: the item's depth and pivot count
         const long long pc0 = (p.prof && tid == 0) ? clock64() : 0;
         if (p.given_rows) {
             d = load_given<BLOCK>(p, rows);
+        } else if (MODE == MODE_PIVOT && p.in_buf) {
+            // spilled item (kind 0, more than kWarpD members): its set's ids
+            // are the locals; the sub-graph induced by them is undirected
+            const uint32_t *it = p.in_buf + p.in_off[s_task];
+            d = int(it[1]);
+            it_s = int(it[2]);
+            it_npv = int(it[3]);
+            for (int i = tid; i < d; i += BLOCK) l2g[i] = int32_t(it[4 + i]);
+            __syncthreads();
+            rows_from_locals<BLOCK>(p, l2g, d, rows, scratch, false, bytes);
         } else {
             const int32_t task = p.tasks[s_task];
             const bool need_rows = MODE == MODE_EXTRACT || MODE == MODE_PIVOT || t >= 2;
@@ -509,6 +556,14 @@ __global__ void __launch_bounds__(BLOCK) k_count(CountParams p) {
                 p.extract_rows[i] = rows[r * RS + w];
             }
             if (tid == 0) *p.extract_d = d;
+            continue;
+        }
+        if (MODE == MODE_PIVOT && p.in_buf) {
+            // an item is a node inside a counted task: no task, no visit here
+            const ull wt0 = work;
+            pivot_task<BLOCK, WPL>(p, rows, d, S0, P0, F, list, SS, sink, q, &s_next, &s_piv0,
+                                   s_key, visits, work, it_s, it_npv);
+            work = wt0 + (work - wt0) * ull((d + 31) >> 5);
             continue;
         }
         if (p.split) {
@@ -666,7 +721,7 @@ __global__ void __launch_bounds__(BLOCK) k_count_warp(CountParams p) {
     F.fw = p.fw;
     F.gm = p.frames_global ? p.frames_global + (int64_t(blockIdx.x) * NW + warp) * p.frames_slot
                            : nullptr;
-    __shared__ int s_hc[2 * NW];
+    __shared__ int s_hc[4 * NW];
     kct::PivotLeafSink sink;
     sink.whist = whist;
     sink.g_hist = p.hist;
@@ -674,7 +729,8 @@ __global__ void __launch_bounds__(BLOCK) k_count_warp(CountParams p) {
     sink.gq = (GQ && MODE == MODE_PIVOT) ? &p.gq : nullptr;  // compile-time off when !GQ
     sink.eager = false;
     sink.l2g = l2g;
-    sink.hc = s_hc + 2 * warp;
+    sink.hc = s_hc + 4 * warp;
+    if (MODE == MODE_PIVOT && p.use_spill) sink.sp = &p.spill;
     sink.push_min = p.gq_push_min;
     sink.cooldown = p.gq_cooldown;
     sink.room_min = p.gq_room;
@@ -694,6 +750,44 @@ __global__ void __launch_bounds__(BLOCK) k_count_warp(CountParams p) {
         if (lane == 0) i = atomicAdd(p.task_counter, 1ull);
         i = __shfl_sync(kct::FULL, i, 0);
         if (i >= ull(p.n_tasks)) break;
+        if (sink.sp) sink.set_budget(p.spill_budget, lane);
+        if (MODE == MODE_PIVOT && p.in_buf) {
+            // spill round: walk item i (a node inside a counted task -- no
+            // task, no visit of its own; engine_pivot.py:117-233 from there)
+            const uint32_t *it = p.in_buf + p.in_off[i];
+            const uint32_t kind = __ldg(it), n = __ldg(it + 1);
+            if (kind == 2u) {  // S-tier universe + pending nodes
+                SS.srow[lane] = __ldg(it + 4 + lane);
+                for (int j = lane; j < int(n); j += 32)
+                    SS.nstk[j] = make_uint2(__ldg(it + 36 + 2 * j), __ldg(it + 37 + 2 * j));
+                __syncwarp();
+                kct::pivot_lanes_run(SS.srow, int(n), t, allk, SS.nstk, SS.ncap, sink, lane,
+                                     visits, work);
+            } else {  // global ids of the set: rebuild its undirected sub-graph
+                const int s0 = int(__ldg(it + 2)), npv0 = int(__ldg(it + 3));
+                for (int j = lane; j < int(n); j += 32) l2g[j] = int32_t(__ldg(it + 4 + j));
+                __syncwarp();
+                warp_rows(p, l2g, int(n), rows, false, bytes, SS);
+                const int W = (int(n) + 31) >> 5, RS = row_stride(W);
+                const ull wt0 = work;
+                if (W == 1) {
+                    const uint32_t all = n >= 32 ? kct::FULL : ((1u << n) - 1u);
+                    kct::pivot_lanes(rows, all, s0, npv0, t, allk, SS.nstk, SS.ncap, sink, lane,
+                                     visits, work);
+                } else {
+                    kct::Set<WPL> A;
+                    const int lo = lane << 5;
+                    A.w[0] = lo >= int(n) ? 0u
+                                          : (lo + 32 <= int(n) ? kct::FULL
+                                                               : ((1u << (int(n) - lo)) - 1u));
+                    kct::pivot_from<WPL>(rows, RS, W, t, allk, A, s0, npv0, F, list, SS, sink,
+                                         nullptr, visits, work);
+                }
+                work = wt0 + (work - wt0) * ull(W);
+            }
+            __syncwarp();
+            continue;
+        }
         const int32_t task = p.tasks[i];
         const bool need_rows = MODE == MODE_PIVOT || t >= 2;
         const long long pc0 = (p.prof && lane == 0) ? clock64() : 0;
@@ -1267,6 +1361,7 @@ CtaPlan plan_cta(const CountParams &p) {
         size_t w = (MODE == MODE_PIVOT ? 64 * WPL + kStealCap * (32 * WPL + 4) : 0) +
                    size_t(NW) * (dpad + 32 * WPL + kCtaSmallWords + hist_words +
                                  (MODE == MODE_ORIENT && p.t >= 4 ? kct::mid_words(WPL) : 0) +
+                                 (MODE == MODE_PIVOT ? 2 * kct::kNodeCap : 0) +
                                  size_t(nsm) * p.fw);
         if (p.scheme == KC_SCHEME_EDGE) w = std::max(w, dpad);
         if (MODE != MODE_PIVOT) {
@@ -1437,6 +1532,44 @@ void launch_sync(kc_graph *g, CountParams &p, int grid_override) {
 
 }  // namespace
 
+// Two item buffers for the pivot spill rounds (round r reads one, writes the
+// other).  Capacities: 256M words (1 GB) and 4M items per list per buffer;
+// a full buffer only makes walkers keep their work (kct::Spill).
+constexpr int kSpillBudget = 1 << 16;  // branches per bounded walk (KC_SPILL_BUDGET)
+struct SpillBufs {
+    ull cap_words = 0;
+    uint32_t cap_small = 0, cap_big = 0;
+    std::unique_ptr<DevBuf> words[2], offs[2], ctls;
+    void alloc(kc_graph *g) {
+        size_t free_b = 0, total_b = 0;
+        KC_CUDA(cudaMemGetInfo(&free_b, &total_b));
+        cap_words = std::min<ull>(ull(1) << 28, ull(free_b / 16) / 4);  // <= 1/16 of free HBM
+        cap_small = cap_big = 1u << 22;
+        for (int i = 0; i < 2; ++i) {
+            words[i].reset(new DevBuf(4 * size_t(cap_words), g->stream));
+            offs[i].reset(new DevBuf(4 * (size_t(cap_small) + cap_big), g->stream));
+        }
+        ctls.reset(new DevBuf(2 * 8 * 8, g->stream));
+        KC_CUDA(cudaMemsetAsync(ctls->p, 0, 2 * 8 * 8, g->stream));
+    }
+    ull *ctl(int i) const { return ctls->as<ull>() + 8 * i; }
+    uint32_t *buf(int i) const { return words[i]->as<uint32_t>(); }
+    uint32_t *small_off(int i) const { return offs[i]->as<uint32_t>(); }
+    uint32_t *big_off(int i) const { return offs[i]->as<uint32_t>() + cap_small; }
+    kct::Spill at(int i) const {
+        kct::Spill sp;
+        sp.buf = buf(i);
+        sp.ctl = ctl(i);
+        sp.small_off = small_off(i);
+        sp.big_off = big_off(i);
+        sp.cap_words = cap_words;
+        sp.cap_small = cap_small;
+        sp.cap_big = cap_big;
+        sp.big_thr = kWarpD;
+        return sp;
+    }
+};
+
 // ---------------------------------------------------------------------------
 void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_t *hist,
                  int64_t hist_cap, uint64_t *visits_per_sm, int32_t n_sm) {
@@ -1571,6 +1704,20 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
     p.gq_push_min = env_int("KC_GQ_PUSHMIN", kct::kPushMin);
     p.gq_cooldown = env_int("KC_GQ_COOLDOWN", kct::kPushCooldown);
     p.gq_room = env_int("KC_GQ_ROOM", kct::kPushRoom);
+    // Pivot bounded walks + spill rounds (KC_SPILL=0 turns them off and
+    // leaves the subtree queue in charge of the balance)
+    static const bool spill_on = [] {
+        const char *e = getenv("KC_SPILL");
+        return !(e && e[0] == '0');
+    }();
+    p.use_spill = pivot && spill_on ? 1 : 0;
+    p.spill_budget = env_int("KC_SPILL_BUDGET", kSpillBudget);
+    SpillBufs spb;
+    if (p.use_spill) {
+        spb.alloc(g);
+        p.spill = spb.at(0);
+        p.use_gq = 0;  // the spill rounds replace the subtree queue
+    }
     Keep keep;
     // Edge tasks (and split items) all go to the warp-per-task kernel; the few
     // whose intersection exceeds kWarpD locals are appended to an overflow
@@ -1761,6 +1908,64 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
             b.task_counter = o + 8 + kSmidSlots + 4;
             if (pivot) launch<MODE_PIVOT>(g, b, 0, keep, g->stream);
             else launch<MODE_ORIENT>(g, b, 0, keep, g->stream);
+        }
+    }
+    if (p.use_spill) {
+        // spill rounds: walk the items the previous round handed over (bounded
+        // again), big sets on the CTA tier, the rest on the warp tier, until a
+        // round hands nothing over
+        KC_CUDA(cudaStreamSynchronize(g->aux));
+        KC_CUDA(cudaStreamSynchronize(g->stream));
+        int cur = 0;
+        for (int round = 1;; ++round) {
+            ull hdr[5];
+            KC_CUDA(cudaMemcpy(hdr, spb.ctl(cur), sizeof(hdr), cudaMemcpyDeviceToHost));
+            const int64_t n_small = int64_t(std::min<ull>(hdr[1], spb.cap_small));
+            const int64_t n_big = int64_t(std::min<ull>(hdr[2], spb.cap_big));
+            if (timing_on())
+                fprintf(stderr, "[kc_timing] spill round %d: small %lld big %lld words %llu "
+                        "failed %llu\n", round, (long long)n_small, (long long)n_big,
+                        hdr[0], hdr[3]);
+            if (n_small == 0 && n_big == 0) break;
+            const int nxt = cur ^ 1;
+            KC_CUDA(cudaMemsetAsync(spb.ctl(nxt), 0, 8 * 8, g->stream));
+            keep.emplace_back(new DevBuf(16, g->stream));
+            ull *ctr = keep.back()->as<ull>();
+            KC_CUDA(cudaMemsetAsync(ctr, 0, 16, g->stream));
+            KC_CUDA(cudaEventRecord(e_fork, g->stream));
+            KC_CUDA(cudaStreamWaitEvent(g->aux, e_fork, 0));
+            if (n_big > 0) {
+                CountParams b = p;
+                b.spill = spb.at(nxt);
+                b.in_buf = spb.buf(cur);
+                b.in_off = spb.big_off(cur);
+                b.n_tasks = n_big;
+                b.tasks = nullptr;
+                b.task_w = nullptr;
+                b.split = 0;
+                b.task_counter = ctr;
+                b.dcap = int(std::max<ull>(std::min<ull>(hdr[4], ull(p.dcap)), 1ull));
+                b.wcap = (b.dcap + 31) / 32;
+                launch<MODE_PIVOT>(g, b, 0, keep, g->stream);
+            }
+            if (n_small > 0) {
+                CountParams q = p;
+                q.spill = spb.at(nxt);
+                q.in_buf = spb.buf(cur);
+                q.in_off = spb.small_off(cur);
+                q.n_tasks = n_small;
+                q.tasks = nullptr;
+                q.task_w = nullptr;
+                q.split = 0;
+                q.branch = 0;
+                q.roots_only = 0;
+                q.task_counter = ctr + 1;
+                launch_warp<MODE_PIVOT>(g, q, keep, g->aux);
+            }
+            KC_CUDA(cudaStreamSynchronize(g->aux));
+            KC_CUDA(cudaStreamSynchronize(g->stream));
+            cur = nxt;
+            KC_REQUIRE(round < 100000, KC_ECUDA, "spill rounds do not terminate");
         }
     }
     KC_CUDA(cudaEventRecord(e_join, g->aux));

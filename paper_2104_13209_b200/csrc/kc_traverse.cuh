@@ -303,6 +303,83 @@ struct CsaAcc {
     }
 };
 
+// Pair level with one lane per member and DYNAMIC assignment: a lane that
+// has walked all of its member's X_v = C & row v takes the next unassigned
+// member, so the warp stays busy until the pool is dry (chunks of 32
+// members ran at ~20 of 32 active lanes: ncu, profiles/r2b_ncu_cta_*).
+// NWD-word rows with an NWD-word stride (16- or 32-byte loads); members are
+// list[0..n) (or 0..n-1 when list is null).  One carry-save accumulator
+// collects every pair's popc(X_v & row x); counts and visits are sums.
+template <int NWD>
+__device__ __forceinline__ void pick_top_word(const uint32_t (&cm)[NWD], int below, int &wcur,
+                                              uint32_t &cur) {
+    int nw = -1;
+    uint32_t nc = 0u;
+#pragma unroll
+    for (int k = 0; k < NWD; ++k)
+        if (k < below && cm[k]) {
+            nw = k;
+            nc = cm[k];
+        }
+    wcur = nw;
+    cur = nc;
+}
+
+template <int NWD>
+__device__ __forceinline__ void score_pairs_dyn(const uint32_t *__restrict__ rows,
+                                                const uint32_t (&c)[NWD], const int *list, int n,
+                                                int lane, ull &acc, ull &visits, ull &work) {
+    uint32_t cm[NWD];
+    uint32_t cur = 0u;
+    int wcur = -1;
+    unsigned vis = 0, wk = 0;
+    CsaAcc h;
+    auto load = [&](int idx) {
+        const int v = list ? list[idx] : idx;
+        const uint32_t *rv = rows + v * NWD;
+        unsigned xs = 0;
+#pragma unroll
+        for (int q = 0; q < NWD; q += 4) {
+            const uint4 r = *reinterpret_cast<const uint4 *>(rv + q);
+            cm[q] = c[q] & r.x;
+            cm[q + 1] = c[q + 1] & r.y;
+            cm[q + 2] = c[q + 2] & r.z;
+            cm[q + 3] = c[q + 3] & r.w;
+        }
+#pragma unroll
+        for (int q = 0; q < NWD; ++q) xs += unsigned(__popc(cm[q]));
+        vis += xs;
+        wk += 1u + xs;
+        pick_top_word<NWD>(cm, NWD, wcur, cur);
+    };
+    if (lane < n) load(lane);
+    int next = 32;  // uniform: next member to hand out
+    for (;;) {
+        unsigned needy = __ballot_sync(FULL, wcur < 0);
+        while (needy && next < n) {
+            const int rank = __popc(needy & ((1u << lane) - 1u));
+            if (wcur < 0 && next + rank < n) load(next + rank);
+            next += __popc(needy);
+            needy = __ballot_sync(FULL, wcur < 0);
+        }
+        if (__ballot_sync(FULL, wcur >= 0) == 0u) break;
+        if (wcur >= 0) {
+            const int b = 31 - __clz(cur);
+            cur ^= 1u << b;
+            const uint32_t *rx = rows + ((wcur << 5) + b) * NWD;
+#pragma unroll
+            for (int q = 0; q < NWD; q += 4) {
+                const uint4 r = *reinterpret_cast<const uint4 *>(rx + q);
+                h.add4(cm[q] & r.x, cm[q + 1] & r.y, cm[q + 2] & r.z, cm[q + 3] & r.w);
+            }
+            if (!cur) pick_top_word<NWD>(cm, wcur, wcur, cur);
+        }
+    }
+    acc += h.total();
+    visits += vis;
+    work += wk;
+}
+
 // Warp tier, rows of at most four words with a 16-byte stride: the members v
 // of C are spread so that each gets 32 / pow2ceil(#members) lanes (a sub-warp
 // group), and the lanes of a group split v's walk over X_v = C & row v by
@@ -315,6 +392,12 @@ __device__ __forceinline__ void score_pairs4(const uint32_t *__restrict__ rows, 
     const uint32_t c2 = __shfl_sync(FULL, C.w[0], 2), c3 = __shfl_sync(FULL, C.w[0], 3);
     const int n = compact4(c0, c1, c2, c3, list, lane);
     if (lane == 0) visits += ull(n);
+    if (n > 16) {  // one lane per member, dynamically assigned
+        const uint32_t c[4] = {c0, c1, c2, c3};
+        score_pairs_dyn<4>(rows, c, list, n, lane, acc, visits, work);
+        __syncwarp();
+        return;
+    }
     unsigned a32 = 0;
     for (int base = 0; base < n; base += 32) {
         const int cnt = n - base < 32 ? n - base : 32;
@@ -358,6 +441,11 @@ __device__ __forceinline__ void score_pairs8(const uint32_t *__restrict__ rows, 
         c[i] = lo >= n ? 0u : (lo + 32 <= n ? FULL : ((1u << (n - lo)) - 1u));
     }
     if (lane == 0) visits += ull(n);
+    if (n > 16) {  // one lane per member, dynamically assigned
+        score_pairs_dyn<8>(rows, c, nullptr, n, lane, acc, visits, work);
+        __syncwarp();
+        return;
+    }
     unsigned a32 = 0;
     for (int base = 0; base < n; base += 32) {
         const int cnt = n - base < 32 ? n - base : 32;
@@ -978,6 +1066,48 @@ struct GQueue {
     __device__ __forceinline__ void set(int i, int v) const { *(volatile int *)(ctl + i) = v; }
 };
 
+// ---------------------------------------------------------------------------
+// Bounded pivot walks with spilling (round-based work distribution).  A walk
+// (one task, or one spilled item) may expand at most `budget` branches; past
+// that, every pending child -- the frames' remaining branches, the per-lane
+// node stack -- is written out as a self-contained ITEM instead of being
+// walked, and the next round's launches walk the items (again bounded).  A
+// subtree of X depends only on the sub-graph induced by X and on (depth,
+// pivot count), so visits and leaves are exactly the unbounded walk's
+// (engine_pivot.py:117-233); only who walks which subtree changes.  Items:
+//   kind 0: [0, n, s, npv] + the n global vertex ids of X, ascending;
+//           n <= big_thr -> small list (warp tier), else big list (CTA tier)
+//   kind 2: [2, m, 0, 0] + 32 compressed rows + m nodes (C, s | npv << 16)
+//           of one S-tier universe (the per-lane walk's pending stack)
+// Offsets are appended with atomics; a full buffer makes the emitter walk
+// the child itself (never lost, only slower).
+// ---------------------------------------------------------------------------
+constexpr int kSpillBatch = 64;  // S-tier nodes per kind-2 item
+struct Spill {
+    uint32_t *buf;     // item words
+    ull *ctl;          // [0] word cursor [1] small items [2] big items [3] failed [4] max big n
+    uint32_t *small_off, *big_off;
+    ull cap_words;
+    uint32_t cap_small, cap_big;
+    int big_thr;
+    // lane 0: reserve an item of `words` words; ~0u when full
+    __device__ __forceinline__ uint32_t reserve(int words, bool big, int n) const {
+        const ull off = atomicAdd(&ctl[0], ull(words));
+        if (off + ull(words) > cap_words) {
+            atomicAdd(&ctl[3], 1ull);
+            return 0xffffffffu;
+        }
+        const ull idx = atomicAdd(&ctl[big ? 2 : 1], 1ull);
+        if (idx >= ull(big ? cap_big : cap_small)) {
+            atomicAdd(&ctl[3], 1ull);
+            return 0xffffffffu;
+        }
+        (big ? big_off : small_off)[idx] = uint32_t(off);
+        if (big) atomicMax(&ctl[4], ull(n));
+        return uint32_t(off);
+    }
+};
+
 struct PivotLeafSink {
     uint32_t *whist;  // this warp's kLeafCells counters
     ull *g_hist;      // global L x L histogram
@@ -988,6 +1118,66 @@ struct PivotLeafSink {
     const int32_t *l2g;  // local id -> global vertex id of the current universe
     int *hc;             // per-warp smem: [0] countdown [1] cached hungry
     int push_min = kPushMin, cooldown = kPushCooldown, room_min = kPushRoom;
+    // bounded walks (nullptr: unbounded).  hc[2] = remaining budget of this
+    // warp's walk, hc[3] = 1 after a failed emission (walk on unbounded);
+    // cta_flag: CTA tier -- once one warp of the task is over budget, all are
+    const Spill *sp = nullptr;
+    int *cta_flag = nullptr;
+    __device__ __forceinline__ void set_budget(int b, int lane) const {
+        if (lane == 0) {
+            hc[2] = b;
+            hc[3] = 0;
+        }
+        __syncwarp();
+    }
+    // uniform: charge n expanded branches; true once the budget is spent
+    __device__ __forceinline__ bool spend(int n, int lane) const {
+        if (!sp) return false;
+        int r = 0;
+        if (lane == 0) {
+            if (hc[3]) {
+                r = 1;
+            } else {
+                r = (hc[2] -= n);
+                if (cta_flag) {
+                    if (r < 0) *(volatile int *)cta_flag = 1;
+                    else if (*(volatile int *)cta_flag) r = -1;
+                }
+            }
+        }
+        return __shfl_sync(0xffffffffu, r, 0) < 0;
+    }
+    __device__ __forceinline__ void no_spill(int lane) const {
+        if (lane == 0) hc[3] = 1;
+        __syncwarp();
+    }
+    // kind-0 item: the global ids of X (lane-distributed over this universe)
+    template <int WPL>
+    __device__ __forceinline__ bool spill_ids(const Set<WPL> &X, int n, int s, int npv, int *list,
+                                              int lane) const;
+    // kind-2 item: an S-tier universe (32 compressed rows) with nb pending nodes
+    __device__ __forceinline__ bool spill_batch(const uint32_t *srow, const uint2 *nodes, int nb,
+                                                int lane) const {
+        uint32_t off = 0;
+        if (lane == 0) off = sp->reserve(4 + 32 + 2 * nb, false, 0);
+        off = __shfl_sync(0xffffffffu, off, 0);
+        if (off == 0xffffffffu) return false;
+        uint32_t *it = sp->buf + off;
+        if (lane == 0) {
+            it[0] = 2u;
+            it[1] = uint32_t(nb);
+            it[2] = 0u;
+            it[3] = 0u;
+        }
+        it[4 + lane] = srow[lane];
+        for (int i = lane; i < nb; i += 32) {
+            const uint2 nd = nodes[i];
+            it[36 + 2 * i] = nd.x;
+            it[37 + 2 * i] = nd.y;
+        }
+        __syncwarp();
+        return true;
+    }
     // uniform: should a child of n members be handed to a hungry warp?
     // Rate-limited: at most one hand-over per kPushCooldown decisions, so a
     // donor keeps doing its own work and thieves get substantial subtrees.
@@ -1103,6 +1293,27 @@ struct PivotLeafSink {
         __syncwarp();
     }
 };
+
+template <int WPL>
+__device__ __forceinline__ bool PivotLeafSink::spill_ids(const Set<WPL> &X, int n, int s, int npv,
+                                                        int *list, int lane) const {
+    const bool big = n > sp->big_thr;
+    uint32_t off = 0;
+    if (lane == 0) off = sp->reserve(4 + n, big, n);
+    off = __shfl_sync(0xffffffffu, off, 0);
+    if (off == 0xffffffffu) return false;
+    compact<WPL>(X, list, lane);
+    uint32_t *it = sp->buf + off;
+    if (lane == 0) {
+        it[0] = 0u;
+        it[1] = uint32_t(n);
+        it[2] = uint32_t(s);
+        it[3] = uint32_t(npv);
+    }
+    for (int i = lane; i < n; i += 32) it[4 + i] = uint32_t(l2g[list[i]]);
+    __syncwarp();
+    return true;
+}
 
 // Take the lowest pending branch v of the shallowest stored frame (lane j
 // holds frame s0+j; `depth` frames are stored) and hand its child to the
@@ -1223,17 +1434,29 @@ __device__ void pivot_small(const uint32_t *srow, uint32_t myrow, uint32_t C, in
 // nearly full a node's subtree is walked by the uniform path instead; while
 // some warp is hungry the bottom (shallowest) node is handed to the GPU-wide
 // queue as a compressed item.
+// nstk[0..size) already holds the pending nodes (a spilled batch, or the root)
 template <typename Sink>
-__device__ void pivot_lanes(const uint32_t *srow, uint32_t C0, int s0, int npv0, int t, bool allk,
-                            uint2 *nstk, int ncap, const Sink &sink, int lane, ull &visits,
-                            ull &work) {
-    if (lane == 0) nstk[0] = make_uint2(C0, uint32_t(s0) | (uint32_t(npv0) << 16));
-    __syncwarp();
-    int size = 1;  // uniform
-    unsigned vis = 0, wk = 0;
+__device__ void pivot_lanes_run(const uint32_t *srow, int size, int t, bool allk, uint2 *nstk,
+                                int ncap, const Sink &sink, int lane, ull &visits, ull &work) {
+    unsigned vis = 0, wk = 0, vis0 = 0;
     const uint32_t myrow = srow[lane];
     for (;;) {
         if (size == 0) break;
+        if (sink.sp) {
+            // bounded walk: charge the previous round's branches; once the
+            // budget is spent the whole pending stack leaves as kind-2 items
+            const int rv = int(__reduce_add_sync(FULL, vis - vis0));
+            vis0 = vis;
+            if (sink.spend(rv, lane)) {
+                while (size > 0) {
+                    const int nb = size < kSpillBatch ? size : kSpillBatch;
+                    if (!sink.spill_batch(srow, nstk + size - nb, nb, lane)) break;
+                    size -= nb;
+                }
+                if (size == 0) break;
+                sink.no_spill(lane);  // buffer full: walk the rest here
+            }
+        }
         if (sink.gq && size >= 2 && sink.want_push(sink.push_min, 1 << 20, lane)) {
             const uint2 nb = nstk[0];  // bottom: the shallowest pending node
             if (__popc(nb.x) >= sink.push_min &&
@@ -1326,6 +1549,15 @@ __device__ void pivot_lanes(const uint32_t *srow, uint32_t C0, int s0, int npv0,
     }
     visits += vis;
     work += ull(vis) + wk;
+}
+
+template <typename Sink>
+__device__ void pivot_lanes(const uint32_t *srow, uint32_t C0, int s0, int npv0, int t, bool allk,
+                            uint2 *nstk, int ncap, const Sink &sink, int lane, ull &visits,
+                            ull &work) {
+    if (lane == 0) nstk[0] = make_uint2(C0, uint32_t(s0) | (uint32_t(npv0) << 16));
+    __syncwarp();
+    pivot_lanes_run(srow, 1, t, allk, nstk, ncap, sink, lane, visits, work);
 }
 
 // ---------------------------------------------------------------------------
@@ -1652,6 +1884,13 @@ __device__ void pivot_from(const uint32_t *__restrict__ rows, int RS, int W, int
     const int lane = threadIdx.x & 31;
     if (pivot_try_small<WPL>(rows, RS, W, C, s0, npv, t, allk, list, SS, sink, lane, visits, work))
         return;
+    if (sink.sp && sink.spend(0, lane)) {
+        // this walk's budget is already spent: hand C itself over
+        if (sink.spill_ids<WPL>(C, warp_count<WPL>(C), s0, npv, list, lane)) return;
+        sink.no_spill(lane);
+    }
+    int pend = 0;           // branches not yet charged to the budget (uniform)
+    bool spilling = false;  // budget spent: children leave as items
     const int PO = 32 * WPL, SC = 64 * WPL;  // P offset, scalars offset
     int s = s0;
     int piv = select_pivot<WPL>(rows, RS, C, list, lane, work, W);
@@ -1695,6 +1934,10 @@ __device__ void pivot_from(const uint32_t *__restrict__ rows, int RS, int W, int
             ++visits;
             work += 1;
         }
+        if (sink.sp && !spilling && ++pend >= 16) {
+            spilling = sink.spend(pend, lane);
+            pend = 0;
+        }
         Set<WPL> X;
         const uint32_t *rv = rows + v * RS;
 #pragma unroll
@@ -1706,6 +1949,16 @@ __device__ void pivot_from(const uint32_t *__restrict__ rows, int RS, int W, int
         if (any_set<WPL>(X)) {
             // a child whose every branch would be pruned adds neither visits nor leaves
             if (!allk && s + 2 - t > np2 + 1) continue;
+            if (spilling) {
+                // over budget: the child leaves as an item instead of being
+                // walked (<= 32 members: the S-tier walk below spills it)
+                const int nx = warp_count<WPL>(X);
+                if (nx > 32) {
+                    if (sink.spill_ids<WPL>(X, nx, s + 1, np2, list, lane)) continue;
+                    sink.no_spill(lane);
+                    spilling = false;
+                }
+            }
             {
                 const int nx = warp_count<WPL>(X);
                 if (WPL == 1 && sink.want_push(nx, allk ? 1 << 20 : t - s0, lane)) {
@@ -1756,10 +2009,12 @@ __device__ void pivot_subtree(const uint32_t *__restrict__ rows, int RS, int W, 
                               int v0, int piv0, const uint32_t *S0, const uint32_t *P0,
                               const Frames &F, int *list, const SmallScratch &SS,
                               const PivotLeafSink &sink, ull &visits, ull &work,
-                              const StealStack *q = nullptr) {
+                              const StealStack *q = nullptr, int s0 = 0, int npv0 = 0) {
+    // (s0, npv0): depth and pivot count of the frame S0 (0, 0 for a task root;
+    // a spilled item's node otherwise)
     const int lane = threadIdx.x & 31;
-    const int np0 = v0 == piv0 ? 1 : 0;
-    if (!allk && 1 - t > np0) return;  // engine_pivot.py:152-153
+    const int np0 = npv0 + (v0 == piv0 ? 1 : 0);
+    if (!allk && s0 + 1 - t > np0) return;  // engine_pivot.py:152-153
     if (lane == 0) {
         ++visits;
         work += 1;
@@ -1774,11 +2029,11 @@ __device__ void pivot_subtree(const uint32_t *__restrict__ rows, int RS, int W, 
         }
     }
     if (!any_set<WPL>(C)) {
-        if ((allk || 1 >= t) && lane == 0) sink.add(1, np0);
+        if ((allk || s0 + 1 >= t) && lane == 0) sink.add(s0 + 1, np0);
         return;
     }
-    if (!allk && 2 - t > np0 + 1) return;  // dead child
-    pivot_from<WPL>(rows, RS, W, t, allk, C, 1, np0, F, list, SS, sink, q, visits, work);
+    if (!allk && s0 + 2 - t > np0 + 1) return;  // dead child
+    pivot_from<WPL>(rows, RS, W, t, allk, C, s0 + 1, np0, F, list, SS, sink, q, visits, work);
 }
 
 // Idle loop of the work-sharing protocol: pop and walk stolen subtrees until

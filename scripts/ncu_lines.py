@@ -23,7 +23,8 @@ for r in rows:
     try:
         s = float(r[4] or 0)
         ex = float(r[7] or 0)
-        th = float(r[10] or 0) if r[10] not in ("-", "") else 0.0
+        tix = float(r[8] or 0) if r[8] not in ("-", "") else 0.0
+        th = tix / ex if ex else 0.0  # average active threads per executed instruction
     except ValueError:
         continue
     lines.append((s, fname, r[0], r[1].strip()[:90], ex, th))
