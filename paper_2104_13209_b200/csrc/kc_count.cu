@@ -1533,7 +1533,7 @@ void launch_sync(kc_graph *g, CountParams &p, int grid_override) {
 }  // namespace
 
 // Two item buffers for the pivot spill rounds (round r reads one, writes the
-// other).  Capacities: 256M words (1 GB) and 4M items per list per buffer;
+// other).  Capacities: 1G words (4 GB) and 16M items per list per buffer;
 // a full buffer only makes walkers keep their work (kct::Spill).
 constexpr int kSpillBudget = 1 << 16;  // branches per bounded walk (KC_SPILL_BUDGET)
 struct SpillBufs {
@@ -1543,8 +1543,8 @@ struct SpillBufs {
     void alloc(kc_graph *g) {
         size_t free_b = 0, total_b = 0;
         KC_CUDA(cudaMemGetInfo(&free_b, &total_b));
-        cap_words = std::min<ull>(ull(1) << 28, ull(free_b / 16) / 4);  // <= 1/16 of free HBM
-        cap_small = cap_big = 1u << 22;
+        cap_words = std::min<ull>(ull(1) << 30, ull(free_b / 8) / 4);  // <= 1/8 of free HBM
+        cap_small = cap_big = 1u << 24;
         for (int i = 0; i < 2; ++i) {
             words[i].reset(new DevBuf(4 * size_t(cap_words), g->stream));
             offs[i].reset(new DevBuf(4 * (size_t(cap_small) + cap_big), g->stream));
@@ -1925,8 +1925,17 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
             if (timing_on())
                 fprintf(stderr, "[kc_timing] spill round %d: small %lld big %lld words %llu "
                         "failed %llu\n", round, (long long)n_small, (long long)n_big,
-                        hdr[0], hdr[3]);
+                        hdr[0], hdr[3]), fflush(stderr);
             if (n_small == 0 && n_big == 0) break;
+            // budget of this round: small while few items are in flight (the
+            // tail, where one long walk would idle the GPU), larger when the
+            // items far outnumber the warps -- fewer, bigger spills keep the
+            // item count (and the per-item rebuild cost) bounded
+            const int64_t warps = int64_t(g->num_sms) * 16;
+            const int64_t scale = std::max<int64_t>(1, (n_small + n_big) / (4 * warps));
+            const int round_budget =
+                int(std::min<int64_t>(int64_t(p.spill_budget) * std::min<int64_t>(scale, 64),
+                                      int64_t(1) << 30));
             const int nxt = cur ^ 1;
             KC_CUDA(cudaMemsetAsync(spb.ctl(nxt), 0, 8 * 8, g->stream));
             keep.emplace_back(new DevBuf(16, g->stream));
@@ -1937,6 +1946,7 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
             if (n_big > 0) {
                 CountParams b = p;
                 b.spill = spb.at(nxt);
+                b.spill_budget = round_budget;
                 b.in_buf = spb.buf(cur);
                 b.in_off = spb.big_off(cur);
                 b.n_tasks = n_big;
@@ -1951,6 +1961,7 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
             if (n_small > 0) {
                 CountParams q = p;
                 q.spill = spb.at(nxt);
+                q.spill_budget = round_budget;
                 q.in_buf = spb.buf(cur);
                 q.in_off = spb.small_off(cur);
                 q.n_tasks = n_small;

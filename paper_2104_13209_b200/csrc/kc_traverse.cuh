@@ -303,83 +303,6 @@ struct CsaAcc {
     }
 };
 
-// Pair level with one lane per member and DYNAMIC assignment: a lane that
-// has walked all of its member's X_v = C & row v takes the next unassigned
-// member, so the warp stays busy until the pool is dry (chunks of 32
-// members ran at ~20 of 32 active lanes: ncu, profiles/r2b_ncu_cta_*).
-// NWD-word rows with an NWD-word stride (16- or 32-byte loads); members are
-// list[0..n) (or 0..n-1 when list is null).  One carry-save accumulator
-// collects every pair's popc(X_v & row x); counts and visits are sums.
-template <int NWD>
-__device__ __forceinline__ void pick_top_word(const uint32_t (&cm)[NWD], int below, int &wcur,
-                                              uint32_t &cur) {
-    int nw = -1;
-    uint32_t nc = 0u;
-#pragma unroll
-    for (int k = 0; k < NWD; ++k)
-        if (k < below && cm[k]) {
-            nw = k;
-            nc = cm[k];
-        }
-    wcur = nw;
-    cur = nc;
-}
-
-template <int NWD>
-__device__ __forceinline__ void score_pairs_dyn(const uint32_t *__restrict__ rows,
-                                                const uint32_t (&c)[NWD], const int *list, int n,
-                                                int lane, ull &acc, ull &visits, ull &work) {
-    uint32_t cm[NWD];
-    uint32_t cur = 0u;
-    int wcur = -1;
-    unsigned vis = 0, wk = 0;
-    CsaAcc h;
-    auto load = [&](int idx) {
-        const int v = list ? list[idx] : idx;
-        const uint32_t *rv = rows + v * NWD;
-        unsigned xs = 0;
-#pragma unroll
-        for (int q = 0; q < NWD; q += 4) {
-            const uint4 r = *reinterpret_cast<const uint4 *>(rv + q);
-            cm[q] = c[q] & r.x;
-            cm[q + 1] = c[q + 1] & r.y;
-            cm[q + 2] = c[q + 2] & r.z;
-            cm[q + 3] = c[q + 3] & r.w;
-        }
-#pragma unroll
-        for (int q = 0; q < NWD; ++q) xs += unsigned(__popc(cm[q]));
-        vis += xs;
-        wk += 1u + xs;
-        pick_top_word<NWD>(cm, NWD, wcur, cur);
-    };
-    if (lane < n) load(lane);
-    int next = 32;  // uniform: next member to hand out
-    for (;;) {
-        unsigned needy = __ballot_sync(FULL, wcur < 0);
-        while (needy && next < n) {
-            const int rank = __popc(needy & ((1u << lane) - 1u));
-            if (wcur < 0 && next + rank < n) load(next + rank);
-            next += __popc(needy);
-            needy = __ballot_sync(FULL, wcur < 0);
-        }
-        if (__ballot_sync(FULL, wcur >= 0) == 0u) break;
-        if (wcur >= 0) {
-            const int b = 31 - __clz(cur);
-            cur ^= 1u << b;
-            const uint32_t *rx = rows + ((wcur << 5) + b) * NWD;
-#pragma unroll
-            for (int q = 0; q < NWD; q += 4) {
-                const uint4 r = *reinterpret_cast<const uint4 *>(rx + q);
-                h.add4(cm[q] & r.x, cm[q + 1] & r.y, cm[q + 2] & r.z, cm[q + 3] & r.w);
-            }
-            if (!cur) pick_top_word<NWD>(cm, wcur, wcur, cur);
-        }
-    }
-    acc += h.total();
-    visits += vis;
-    work += wk;
-}
-
 // Warp tier, rows of at most four words with a 16-byte stride: the members v
 // of C are spread so that each gets 32 / pow2ceil(#members) lanes (a sub-warp
 // group), and the lanes of a group split v's walk over X_v = C & row v by
@@ -392,12 +315,6 @@ __device__ __forceinline__ void score_pairs4(const uint32_t *__restrict__ rows, 
     const uint32_t c2 = __shfl_sync(FULL, C.w[0], 2), c3 = __shfl_sync(FULL, C.w[0], 3);
     const int n = compact4(c0, c1, c2, c3, list, lane);
     if (lane == 0) visits += ull(n);
-    if (n > 16) {  // one lane per member, dynamically assigned
-        const uint32_t c[4] = {c0, c1, c2, c3};
-        score_pairs_dyn<4>(rows, c, list, n, lane, acc, visits, work);
-        __syncwarp();
-        return;
-    }
     unsigned a32 = 0;
     for (int base = 0; base < n; base += 32) {
         const int cnt = n - base < 32 ? n - base : 32;
@@ -441,11 +358,6 @@ __device__ __forceinline__ void score_pairs8(const uint32_t *__restrict__ rows, 
         c[i] = lo >= n ? 0u : (lo + 32 <= n ? FULL : ((1u << (n - lo)) - 1u));
     }
     if (lane == 0) visits += ull(n);
-    if (n > 16) {  // one lane per member, dynamically assigned
-        score_pairs_dyn<8>(rows, c, nullptr, n, lane, acc, visits, work);
-        __syncwarp();
-        return;
-    }
     unsigned a32 = 0;
     for (int base = 0; base < n; base += 32) {
         const int cnt = n - base < 32 ? n - base : 32;

@@ -19,7 +19,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np  # noqa: E402
 import paper_2104_13209_b200 as kc  # noqa: E402
 from paper_2104_13209_b200.orientation import rank_and_orient  # noqa: E402
-from paper_2104_13209_b200.scheduler import device_count_raw  # noqa: E402
+from paper_2104_13209_b200.scheduler import device_count_raw, finalize  # noqa: E402
 from paper_2104_13209_b200.shard import shard_ranges  # noqa: E402
 
 from explore import cached_edges  # noqa: E402
@@ -34,6 +34,8 @@ def main():
     ap.add_argument("--criterion", default="degeneracy")
     ap.add_argument("--world", type=int, default=16)
     ap.add_argument("--ranks", type=int, nargs="+", default=[0])
+    ap.add_argument("--range", type=int, nargs=2, default=None,
+                    help="explicit [lo, hi) of make_tasks order instead of shard ranks")
     a = ap.parse_args()
     g = kc.from_edges(cached_edges(a.workload))
     cfg = kc.RunConfig(k=a.k, algorithm=a.algo, scheme=a.scheme, criterion=a.criterion)
@@ -44,11 +46,14 @@ def main():
     print(json.dumps({"workload": a.workload, "n": g.n, "m": g.m, "d_max": og.d_max,
                       "orient_s": round(orient_s, 3), "world": a.world,
                       "ranges": ranges}), flush=True)
-    for r in a.ranks:
-        lo, hi = ranges[r]
+    todo = [(r, ranges[r]) for r in a.ranks] if a.range is None else [(-1, tuple(a.range))]
+    for r, (lo, hi) in todo:
         t = time.perf_counter()
         raw = device_count_raw(og, cfg, lo, hi)
-        print(json.dumps({"rank": r, "lo": lo, "hi": hi, "wall_s": round(time.perf_counter() - t, 3),
+        count, _ = finalize(raw, cfg, g.n, g.m)
+        print(json.dumps({"rank": r, "lo": lo, "hi": hi, "algo": a.algo, "scheme": a.scheme,
+                          "k": a.k, "count": str(count),
+                          "wall_s": round(time.perf_counter() - t, 3),
                           "kernel_ms": raw.count_ms, "visits": int(raw.visits),
                           "limbs": [int(x) for x in raw.limbs], "word_ops": int(raw.word_ops),
                           "hist_sum": int(np.asarray(raw.hist, dtype=np.uint64).sum()) if raw.hist is not None else 0}),
