@@ -489,12 +489,21 @@ __global__ void __launch_bounds__(BLOCK) k_count(CountParams p) {
     sink.whist = whist;
     sink.g_hist = p.hist;
     sink.L = p.hist_dim;
-    sink.gq = (GQ && MODE == MODE_PIVOT) ? &p.gq : nullptr;  // compile-time off when !GQ
+    // queue / spill descriptors copied to shared memory: taking the address
+    // of a kernel parameter would copy the whole CountParams to local memory
+    __shared__ kct::GQueue s_gq;
+    __shared__ kct::Spill s_sp;
+    if (tid == 0) {
+        s_gq = p.gq;
+        s_sp = p.spill;
+    }
+    __syncthreads();
+    sink.gq = (GQ && MODE == MODE_PIVOT) ? &s_gq : nullptr;  // compile-time off when !GQ
     sink.eager = true;  // CTA tier
     sink.l2g = l2g;
     sink.hc = s_hc + 4 * warp;
     if (MODE == MODE_PIVOT && p.use_spill) {
-        sink.sp = &p.spill;
+        sink.sp = &s_sp;
         sink.cta_flag = &s_spill;
     }
     sink.push_min = p.gq_push_min;
@@ -686,8 +695,10 @@ __device__ int warp_build(const CountParams &p, int32_t task, int32_t *l2g, uint
     return d;
 }
 
+// register budget: the pivot walk keeps up to 128 registers (4 CTAs per SM,
+// the shared-memory limit anyway); the orientation walk 56 (9 CTAs per SM)
 template <int BLOCK, int MODE, bool GQ, int G = 32>
-__global__ void __launch_bounds__(BLOCK) k_count_warp(CountParams p) {
+__global__ void __launch_bounds__(BLOCK, MODE == 1 ? 4 : 9) k_count_warp(CountParams p) {
     constexpr int NW = BLOCK / 32;
     constexpr int D = kWarpD, WPL = 1;
     constexpr int RSD = (D / 32) | 1;
@@ -726,11 +737,18 @@ __global__ void __launch_bounds__(BLOCK) k_count_warp(CountParams p) {
     sink.whist = whist;
     sink.g_hist = p.hist;
     sink.L = p.hist_dim;
-    sink.gq = (GQ && MODE == MODE_PIVOT) ? &p.gq : nullptr;  // compile-time off when !GQ
+    __shared__ kct::GQueue s_gq;  // (see k_count: no address of a kernel parameter)
+    __shared__ kct::Spill s_sp;
+    if (tid == 0) {
+        s_gq = p.gq;
+        s_sp = p.spill;
+    }
+    __syncthreads();
+    sink.gq = (GQ && MODE == MODE_PIVOT) ? &s_gq : nullptr;  // compile-time off when !GQ
     sink.eager = false;
     sink.l2g = l2g;
     sink.hc = s_hc + 4 * warp;
-    if (MODE == MODE_PIVOT && p.use_spill) sink.sp = &p.spill;
+    if (MODE == MODE_PIVOT && p.use_spill) sink.sp = &s_sp;
     sink.push_min = p.gq_push_min;
     sink.cooldown = p.gq_cooldown;
     sink.room_min = p.gq_room;
@@ -903,7 +921,7 @@ __global__ void __launch_bounds__(BLOCK) k_count_warp(CountParams p) {
     }
     if (GQ && MODE == MODE_PIVOT) {
         // task queue drained: serve subtrees handed over by busy warps
-        const kct::GQueue &q = p.gq;
+        const kct::GQueue &q = s_gq;
         if (lane == 0) {  // busy -> hungry (atomics only: no lock storm at the tail)
             atomicAdd(q.ctl + 2, 1);
             atomicSub(q.ctl + 3, 1);

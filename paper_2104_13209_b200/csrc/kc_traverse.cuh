@@ -34,6 +34,25 @@ namespace kct {
 typedef unsigned long long ull;
 constexpr unsigned FULL = 0xffffffffu;
 
+// explicit shared-memory accesses for data the compiler only sees through
+// generic pointers (it would emit LD.E / ST.E with long-scoreboard waits)
+__device__ __forceinline__ unsigned smem_addr(const void *p) {
+    return unsigned(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint32_t lds32(unsigned a) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ uint2 lds64(unsigned a) {
+    uint2 v;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts64(unsigned a, uint2 v) {
+    asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(a), "r"(v.x), "r"(v.y) : "memory");
+}
+
 template <int WPL>
 struct Set {
     uint32_t w[WPL];
@@ -1351,11 +1370,18 @@ template <typename Sink>
 __device__ void pivot_lanes_run(const uint32_t *srow, int size, int t, bool allk, uint2 *nstk,
                                 int ncap, const Sink &sink, int lane, ull &visits, ull &work) {
     unsigned vis = 0, wk = 0, vis0 = 0;
-    const uint32_t myrow = srow[lane];
+    // srow and nstk live in shared memory: explicit ld/st.shared (through the
+    // generic pointers the compiler emitted LD.E, long-scoreboard waits)
+    const unsigned sb = smem_addr(srow), nb0 = smem_addr(nstk);
+    auto row = [&](int v) { return lds32(sb + 4u * unsigned(v)); };
+    auto node = [&](int i) { return lds64(nb0 + 8u * unsigned(i)); };
+    const uint32_t myrow = row(lane);
+    const bool sp_on = sink.sp != nullptr, gq_on = sink.gq != nullptr;
+    int rounds = 0;
     for (;;) {
         if (size == 0) break;
-        if (sink.sp) {
-            // bounded walk: charge the previous round's branches; once the
+        if (sp_on && (++rounds & 7) == 0) {
+            // bounded walk: charge the branches of the last 8 rounds; once the
             // budget is spent the whole pending stack leaves as kind-2 items
             const int rv = int(__reduce_add_sync(FULL, vis - vis0));
             vis0 = vis;
@@ -1369,38 +1395,47 @@ __device__ void pivot_lanes_run(const uint32_t *srow, int size, int t, bool allk
                 sink.no_spill(lane);  // buffer full: walk the rest here
             }
         }
-        if (sink.gq && size >= 2 && sink.want_push(sink.push_min, 1 << 20, lane)) {
-            const uint2 nb = nstk[0];  // bottom: the shallowest pending node
+        if (gq_on && size >= 2 && sink.want_push(sink.push_min, 1 << 20, lane)) {
+            const uint2 nb = node(0);  // bottom: the shallowest pending node
             if (__popc(nb.x) >= sink.push_min &&
                 sink.push_compressed(srow, nb.x, int(nb.y & 0xffffu), int(nb.y >> 16), lane)) {
                 __syncwarp();
-                if (lane == 0) nstk[0] = nstk[size - 1];
+                if (lane == 0) sts64(nb0, node(size - 1));
                 __syncwarp();
                 --size;
                 continue;
             }
         }
         const int free_slots = ncap - size;
-        if (free_slots < 33) {
-            // no room for another round: walk the top node uniformly
-            const uint2 nd = nstk[size - 1];
-            __syncwarp();
+        // take the top k nodes whose children fit: a node pushes at most |C|
+        // children (its branches are members of C), so k is the longest run
+        // of top nodes with sum |C| <= free slots (deep nodes are small: most
+        // rounds run all 32 lanes; the old bound of 32 children per node
+        // allowed at most ncap / 32 = 16)
+        const int cand = size < 32 ? size : 32;
+        const uint2 ndc = lane < cand ? node(size - 1 - lane) : make_uint2(0u, 0u);
+        int need = lane < cand ? __popc(ndc.x) : (1 << 20);
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(FULL, need, o);
+            if (lane >= o) need += y;
+        }
+        const int k = __popc(__ballot_sync(FULL, need <= free_slots));
+        if (k == 0) {
+            // no room for the top node's children: walk it uniformly
+            const uint32_t tc = __shfl_sync(FULL, ndc.x, 0), ty = __shfl_sync(FULL, ndc.y, 0);
             --size;
-            pivot_small(srow, myrow, nd.x, int(nd.y & 0xffffu), int(nd.y >> 16), t, allk, nullptr,
-                        sink, lane, visits, work);
+            pivot_small(srow, myrow, tc, int(ty & 0xffffu), int(ty >> 16), t, allk, nullptr, sink,
+                        lane, visits, work);
             continue;
         }
-        int k = free_slots / 32;  // each expanded node pushes at most 32 children
-        k = k < 32 ? k : 32;
-        k = k < size ? k : size;
         uint32_t C = 0;
         int s = 0, npv = 0;
         const bool have = lane < k;
         if (have) {
-            const uint2 nd = nstk[size - 1 - lane];
-            C = nd.x;
-            s = int(nd.y & 0xffffu);
-            npv = int(nd.y >> 16);
+            C = ndc.x;
+            s = int(ndc.y & 0xffffu);
+            npv = int(ndc.y >> 16);
         }
         size -= k;
         __syncwarp();
@@ -1413,12 +1448,12 @@ __device__ void pivot_lanes_run(const uint32_t *srow, int size, int t, bool allk
             while (m) {
                 const int v = __ffs(m) - 1;
                 m &= m - 1u;
-                const unsigned key = ((unsigned(__popc(C & srow[v])) + 1u) << 5) | unsigned(31 - v);
+                const unsigned key = ((unsigned(__popc(C & row(v))) + 1u) << 5) | unsigned(31 - v);
                 best = key > best ? key : best;
             }
             piv = 31 - int(best & 31u);
             wk += unsigned(__popc(C));
-            P = C & ~srow[piv];
+            P = C & ~row(piv);
             R = (!allk && s + 1 - t > npv) ? (P & (1u << piv)) : P;
             // branches: visits, leaves, and the number of children to push
             uint32_t r = R;
@@ -1428,7 +1463,7 @@ __device__ void pivot_lanes_run(const uint32_t *srow, int size, int t, bool allk
                 const int np2 = npv + (v == piv ? 1 : 0);
                 if (!allk && s + 1 - t > np2) continue;  // pruned: not a visit
                 ++vis;
-                const uint32_t X = C & srow[v] & ~(P & ((1u << v) - 1u));
+                const uint32_t X = C & row(v) & ~(P & ((1u << v) - 1u));
                 if (X) {
                     if (!allk && s + 2 - t > np2 + 1) continue;  // every branch pruned
                     ++nch;
@@ -1452,9 +1487,9 @@ __device__ void pivot_lanes_run(const uint32_t *srow, int size, int t, bool allk
                 r &= r - 1u;
                 const int np2 = npv + (v == piv ? 1 : 0);
                 if (!allk && s + 1 - t > np2) continue;
-                const uint32_t X = C & srow[v] & ~(P & ((1u << v) - 1u));
+                const uint32_t X = C & row(v) & ~(P & ((1u << v) - 1u));
                 if (!X || (!allk && s + 2 - t > np2 + 1)) continue;
-                nstk[at++] = make_uint2(X, uint32_t(s + 1) | (uint32_t(np2) << 16));
+                sts64(nb0 + 8u * unsigned(at++), make_uint2(X, uint32_t(s + 1) | (uint32_t(np2) << 16)));
             }
         }
         __syncwarp();
@@ -1644,7 +1679,7 @@ __device__ __forceinline__ bool pivot_try_small(const uint32_t *__restrict__ row
                                                 ull &work) {
     if (W == 1) {  // rows are already one word: identity relabelling
         const uint32_t c = __shfl_sync(FULL, X.w[0], 0);
-        if (S.nstk && RS == 1) {
+        if (S.nstk && RS == 1 && __isShared(rows)) {  // per-lane walks read rows as shared
             pivot_lanes(rows, c, s, npv, t, allk, S.nstk, S.ncap, sink, lane, visits, work);
             return true;
         }
