@@ -94,6 +94,7 @@ struct CountParams {
     int spill_budget;
     const uint32_t *in_buf;  // spill round: task i is the item at in_buf + in_off[i]
     const uint32_t *in_off;
+    int mid_max;  // CTA tier: largest pair-level set compressed (128 or 256; KC_MID_MAX)
 };
 // prof words: CTA tier build / walk cycles (thread 0), warp tier build / walk
 // cycles (lane 0, summed over warps), then a histogram of overflow task sizes
@@ -460,7 +461,8 @@ __global__ void __launch_bounds__(BLOCK) k_count(CountParams p) {
     if (MODE == MODE_PIVOT) area += 64 * WPL + kStealCap * (32 * WPL + 4);
     const int hist_cells = MODE == MODE_PIVOT ? kct::kLeafCells : 0;
     // compressed pair-level rows: only where a pair level exists (t >= 4)
-    const int mid_words = (MODE == MODE_ORIENT && p.t >= 4) ? kct::mid_words(WPL) : 0;
+    const int mid_words =
+        (MODE == MODE_ORIENT && p.t >= 4) ? kct::mid_words(WPL, p.mid_max) : 0;
     // per-warp S-tier rows only: the CTA tier has no LocalMap (kct::kSmallWords)
     // pivot: per-lane S-tier walks need a node stack per warp
     const int node_words = MODE == MODE_PIVOT ? 2 * kct::kNodeCap : 0;
@@ -472,7 +474,10 @@ __global__ void __launch_bounds__(BLOCK) k_count(CountParams p) {
     SS.srow = cbuf + 32 * WPL;
     SS.sstk = nullptr;  // (unused by the CTA-tier walks)
     uint32_t *whist = SS.srow + kCtaSmallWords;
-    if (mid_words) SS.mrow = whist + hist_cells;  // <= 256-member pair levels
+    if (mid_words) {  // compressed pair levels of <= p.mid_max members
+        SS.mrow = whist + hist_cells;
+        SS.mid_max = p.mid_max;
+    }
     if (node_words) {
         SS.nstk = reinterpret_cast<uint2 *>(whist + hist_cells + mid_words);
         SS.ncap = kct::kNodeCap;
@@ -1378,7 +1383,8 @@ CtaPlan plan_cta(const CountParams &p) {
     auto area_words = [&](int nsm) {
         size_t w = (MODE == MODE_PIVOT ? 64 * WPL + kStealCap * (32 * WPL + 4) : 0) +
                    size_t(NW) * (dpad + 32 * WPL + kCtaSmallWords + hist_words +
-                                 (MODE == MODE_ORIENT && p.t >= 4 ? kct::mid_words(WPL) : 0) +
+                                 (MODE == MODE_ORIENT && p.t >= 4 ? kct::mid_words(WPL, p.mid_max)
+                                                                  : 0) +
                                  (MODE == MODE_PIVOT ? 2 * kct::kNodeCap : 0) +
                                  size_t(nsm) * p.fw);
         if (p.scheme == KC_SCHEME_EDGE) w = std::max(w, dpad);
@@ -1730,6 +1736,9 @@ void kc_do_count(kc_graph *g, const kc_count_args *a, kc_count_raw *raw, uint64_
     }();
     p.use_spill = pivot && spill_on ? 1 : 0;
     p.spill_budget = env_int("KC_SPILL_BUDGET", kSpillBudget);
+    // 256: 8-word rows for 129..256-member pair levels (9 KB per warp);
+    // 128: 2.3 KB per warp, more warps per SM, bigger sets uncompressed
+    p.mid_max = env_int("KC_MID_MAX", 256) <= 128 ? 128 : 256;
     SpillBufs spb;
     if (p.use_spill) {
         spb.alloc(g);

@@ -426,6 +426,9 @@ __device__ __forceinline__ void score_pairs8(const uint32_t *__restrict__ rows, 
 // per (member, word) with no divergence between lanes (the earlier per-bit
 // loop ran at ~2 active lanes: ncu, profiles/r2b_ncu_cta_orient_rmat22.md).
 // Counts and visits are order-free sums, hence unchanged.
+// words of the compressed rows of a pair level of at most mid_max members
+__host__ __device__ constexpr int mid_rows_words(int mid_max) { return mid_max <= 128 ? 512 : 2048; }
+
 __device__ __forceinline__ void compress_masks(uint32_t m, uint32_t (&mv)[5]) {
     uint32_t mk = ~m << 1;
 #pragma unroll
@@ -444,12 +447,12 @@ __device__ __forceinline__ void compress_masks(uint32_t m, uint32_t (&mv)[5]) {
 template <int WPL>
 __device__ __forceinline__ void score_pairs_mid(const uint32_t *__restrict__ rows, int RS, int W,
                                                 const Set<WPL> &X, int *list, uint32_t *cbuf,
-                                                uint32_t *mrow, int lane, ull &acc, ull &visits,
-                                                ull &work) {
+                                                uint32_t *mrow, int mid_max, int lane, ull &acc,
+                                                ull &visits, ull &work) {
     (void)cbuf;
     const int n = compact<WPL>(X, list, lane, W);
     // per word w of X: [X_w, popc(X_w), mv0..mv4, -] (two 16-byte loads)
-    uint32_t *tab = mrow + 256 * 8;
+    uint32_t *tab = mrow + mid_rows_words(mid_max);
 #pragma unroll
     for (int p = 0; p < WPL; ++p) {
         const int w = p * 32 + lane;
@@ -1527,10 +1530,11 @@ struct SmallScratch {
     uint32_t *sstk;  // kMapWords words: LocalMap storage
     uint2 *nstk = nullptr;  // pivot per-lane node stack (warp tier), nullptr: uniform walks
     int ncap = 0;
-    uint32_t *mrow = nullptr;  // mid_words(WPL): compressed <= 256-member pair level (CTA tier)
+    uint32_t *mrow = nullptr;  // mid_words(WPL, mid_max): compressed pair level (CTA tier)
+    int mid_max = 0;           // largest set compressed there (128 or 256)
 };
 // 256 rows of 8 words + the per-word compress table of a set (8 words per word)
-constexpr int mid_words(int wpl) { return 256 * 8 + 8 * 32 * wpl; }
+constexpr int mid_words(int wpl, int mid_max) { return mid_rows_words(mid_max) + 8 * 32 * wpl; }
 constexpr int kNodeCap = 512;  // pivot_lanes stack capacity (nodes of 2 words)
 constexpr int kMapSlots = 256;
 constexpr int kMapWords = kMapSlots + kMapSlots / 4;
@@ -1608,8 +1612,9 @@ __device__ void orient_subtree(const uint32_t *__restrict__ rows, int RS, int W,
     if (orient_try_small<WPL, G>(rows, RS, W, C, 1, last, list, SS, lane, acc, visits, work))
         return;
     if (last == 2) {  // frame 1 is the next-to-last level
-        if (W > 4 && SS.mrow && warp_count<WPL>(C) <= 256)
-            score_pairs_mid<WPL>(rows, RS, W, C, list, cbuf, SS.mrow, lane, acc, visits, work);
+        if (W > 4 && SS.mrow && warp_count<WPL>(C) <= SS.mid_max)
+            score_pairs_mid<WPL>(rows, RS, W, C, list, cbuf, SS.mrow, SS.mid_max, lane, acc,
+                                 visits, work);
         else
             score_pairs<WPL>(rows, RS, W, C, list, cbuf, lane, acc, visits, work);
         return;
@@ -1645,8 +1650,9 @@ __device__ void orient_subtree(const uint32_t *__restrict__ rows, int RS, int W,
                                      work))
             continue;
         if (s + 2 == last) {  // X is the next-to-last frame
-            if (W > 4 && SS.mrow && warp_count<WPL>(X) <= 256)
-                score_pairs_mid<WPL>(rows, RS, W, X, list, cbuf, SS.mrow, lane, acc, visits,
+            if (W > 4 && SS.mrow && warp_count<WPL>(X) <= SS.mid_max)
+                score_pairs_mid<WPL>(rows, RS, W, X, list, cbuf, SS.mrow, SS.mid_max, lane, acc,
+                                     visits,
                                      work);
             else
                 score_pairs<WPL>(rows, RS, W, X, list, cbuf, lane, acc, visits, work);

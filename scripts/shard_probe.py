@@ -50,7 +50,15 @@ def main():
     for r, (lo, hi) in todo:
         t = time.perf_counter()
         raw = device_count_raw(og, cfg, lo, hi)
-        count, _ = finalize(raw, cfg, g.n, g.m)
+        if raw.hist is not None:
+            h = np.asarray(raw.hist)
+            bad = [(int(i), int(j), int(h[i, j])) for i, j in np.argwhere(h) if j > i]
+            if bad:  # a leaf cannot have more pivots than path vertices
+                print(json.dumps({"bad_hist_bins": bad[:20], "n_bad": len(bad)}), flush=True)
+        try:
+            count, _ = finalize(raw, cfg, g.n, g.m)
+        except OverflowError as e:
+            count = f"OverflowError: {e}"
         print(json.dumps({"rank": r, "lo": lo, "hi": hi, "algo": a.algo, "scheme": a.scheme,
                           "k": a.k, "count": str(count),
                           "wall_s": round(time.perf_counter() - t, 3),
