@@ -1782,7 +1782,7 @@ __device__ __forceinline__ void donate_bottom_L(const uint32_t *__restrict__ row
                                                 int lane, ull &visits) {
     const int PO = 32 * WPL, SC = 64 * WPL;
     for (int sf = s0; sf < s_top; ++sf) {
-        uint32_t *f = F.at(sf);
+        uint32_t *f = F.at(sf - s0);
         const Set<WPL> Cf = load_set<WPL>(f, lane), Pf = load_set<WPL>(f + PO, lane);
         const int piv = int(f[SC]), npv = int(f[SC + 1]), c = int(f[SC + 2]);
         Set<WPL> R;
@@ -1842,6 +1842,10 @@ __device__ void pivot_from(const uint32_t *__restrict__ rows, int RS, int W, int
         if (sink.spill_ids<WPL>(C, warp_count<WPL>(C), s0, npv, list, lane)) return;
         sink.no_spill(lane);
     }
+    // frames are indexed relative to the walk's first frame s0: a spilled or
+    // handed-over subtree starts deep in its task's tree (RMAT-22: depth
+    // ~150) while a warp holds frames for one universe (<= its size + 2)
+    auto fr = [&](int x) { return F.at(x - s0); };
     int pend = 0;           // branches not yet charged to the budget (uniform)
     bool spilling = false;  // budget spent: children leave as items
     const int PO = 32 * WPL, SC = 64 * WPL;  // P offset, scalars offset
@@ -1857,7 +1861,7 @@ __device__ void pivot_from(const uint32_t *__restrict__ rows, int RS, int W, int
     // engine_pivot.py:152-153: a frame with deficit npv+1 only branches on its pivot
     if (!allk && s + 1 - t > npv) restrict_to(R, piv, lane);
     {
-        uint32_t *f = F.at(s);
+        uint32_t *f = fr(s);
         store_set<WPL>(f, C, lane);
         store_set<WPL>(f + PO, P, lane);
         if (lane == 0) {
@@ -1870,7 +1874,7 @@ __device__ void pivot_from(const uint32_t *__restrict__ rows, int RS, int W, int
         if (v < 0) {
             if (s == s0) break;
             --s;
-            const uint32_t *f = F.at(s);
+            const uint32_t *f = fr(s);
             C = load_set<WPL>(f, lane);
             P = load_set<WPL>(f + PO, lane);
             piv = int(f[SC]);
@@ -1920,7 +1924,7 @@ __device__ void pivot_from(const uint32_t *__restrict__ rows, int RS, int W, int
                     if (sink.eager) {
                         if (push_large<WPL>(sink, X, list, s + 1, np2, lane)) continue;
                     } else if (s > s0) {
-                        if (lane == 0) F.at(s)[SC + 2] = uint32_t(v);  // cursor of the top frame
+                        if (lane == 0) fr(s)[SC + 2] = uint32_t(v);  // cursor of the top frame
                         __syncwarp();
                         donate_bottom_L<WPL>(rows, RS, W, t, allk, F, s0, s, list, sink, lane,
                                              visits);
@@ -1933,7 +1937,7 @@ __device__ void pivot_from(const uint32_t *__restrict__ rows, int RS, int W, int
             if (pivot_try_small<WPL>(rows, RS, W, X, s + 1, np2, t, allk, list, SS, sink, lane,
                                      visits, work))
                 continue;
-            if (lane == 0) F.at(s)[SC + 2] = uint32_t(v);
+            if (lane == 0) fr(s)[SC + 2] = uint32_t(v);
             ++s;
             npv = np2;
             C = X;
@@ -1943,7 +1947,7 @@ __device__ void pivot_from(const uint32_t *__restrict__ rows, int RS, int W, int
             for (int p = 0; p < WPL; ++p) P.w[p] = C.w[p] & ~rp.w[p];
             R = P;
             if (!allk && s + 1 - t > npv) restrict_to(R, piv, lane);
-            uint32_t *f = F.at(s);
+            uint32_t *f = fr(s);
             store_set<WPL>(f, C, lane);
             store_set<WPL>(f + PO, P, lane);
             if (lane == 0) {
